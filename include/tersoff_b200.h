@@ -1,0 +1,150 @@
+/* tersoff_b200.h — C-ABI of the B200-native Tersoff force/energy path.
+ *
+ * Drop-in boundary for the reference's force path
+ *   tmd::evaluate_forces(const AtomSystem&, const NeighborList&,
+ *                        const ParamTable&, const ForceOptions&) -> EnergyForces
+ *   (/root/reference/proj/include/tmd/potential_opt.hpp:105-106,
+ *    /root/reference/proj/src/potential_opt.cpp:104-138)
+ * and the neighbor-list routines it consumes
+ *   (/root/reference/proj/include/tmd/neighbor.hpp:31-54).
+ *
+ * Plain pointers and sizes only.  Host arrays are owned by the caller.
+ * Positions/forces are AoS double[n][3] exactly like std::vector<Vec3>
+ * (vec3.hpp:9-37); species are int32 (system.hpp:19).
+ *
+ * Return codes mirror the reference's error taxonomy and CLI exit codes
+ * (error.hpp:9-21, tools/main.cpp:241-256):
+ *   TSF_OK 0, TSF_ERR_CONFIG 2 (ConfigError/ParseError), TSF_ERR_NUMERIC 3
+ *   (NumericError), plus TSF_ERR_CUDA 4 and TSF_ERR_INTERNAL 1.
+ * The message of the last failure is available through tsf_last_error(ctx)
+ * or, for calls without a context, tsf_error_message().
+ *
+ * Threading: one CUDA stream per context; a context must not be used from
+ * two threads at once.  Distinct contexts are independent.
+ */
+#ifndef TERSOFF_B200_H
+#define TERSOFF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSF_OK 0
+#define TSF_ERR_INTERNAL 1
+#define TSF_ERR_CONFIG 2
+#define TSF_ERR_NUMERIC 3
+#define TSF_ERR_CUDA 4
+
+/* compute flags */
+#define TSF_DETERMINISTIC 0x1u /* slot buffers + reverse gather: bitwise reproducible  */
+#define TSF_NO_FILTER 0x2u     /* ForceOptions::filter = false (potential_opt.hpp:35) */
+
+/* neighbor-list selectors for tsf_export_neighbors */
+#define TSF_LIST_SKIN 0  /* NeighborList (neighbor.hpp:15-27)              */
+#define TSF_LIST_SHORT 1 /* filter_all_segments output (neighbor.hpp:46-54) */
+
+typedef struct tsf_params tsf_params;
+typedef struct tsf_ctx tsf_ctx;
+
+/* ---- errors ------------------------------------------------------------ */
+const char* tsf_error_message(void);          /* thread-local, context-free calls */
+const char* tsf_last_error(const tsf_ctx* ctx);
+const char* tsf_version(void);
+
+/* ---- parameter table (host only; no GPU needed) -------------------------
+ * Replaces parse_param_text / load_param_file / builtin_silicon /
+ * serialize_param_table (params.hpp:62-75, params.cpp:119-234). */
+int tsf_params_parse(const char* text, size_t len, const char* source_name, tsf_params** out);
+int tsf_params_load(const char* path, tsf_params** out);
+int tsf_params_builtin_silicon(tsf_params** out);
+void tsf_params_free(tsf_params* p);
+int tsf_params_species_count(const tsf_params* p);
+const char* tsf_params_species_name(const tsf_params* p, int species);
+int tsf_params_species_id(const tsf_params* p, const char* name); /* -1 when unknown */
+double tsf_params_r_cut_max(const tsf_params* p);
+/* FlatParams<double> rows (params.hpp:88-115): S^3 rows of 16 doubles. */
+int tsf_params_flat_rows(const tsf_params* p, double* rows, size_t cap);
+/* round-trip-exact text; returns the length (excluding NUL), writes at most cap bytes. */
+int64_t tsf_params_serialize(const tsf_params* p, char* buf, size_t cap);
+
+/* ---- synthetic inputs (host) --------------------------------------------
+ * make_diamond_lattice (engine.hpp:54-55, engine.cpp:28-58),
+ * perturbed_lattice (verify.hpp:24-25, verify.cpp:83-104),
+ * init_velocities (engine.hpp:60, engine.cpp:64-116); bit-identical. */
+int64_t tsf_diamond_lattice_size(int nx, int ny, int nz);
+int tsf_make_diamond_lattice(int nx, int ny, int nz, double a0, int32_t species_id,
+                             double* xyz, int32_t* species, double* box);
+int tsf_perturbed_lattice(const tsf_params* p, int cells, double jitter, uint64_t seed,
+                          double* xyz, int32_t* species, double* masses /* S */, double* box);
+int tsf_init_velocities(int64_t n, const int32_t* species, const double* masses,
+                        double temperature, uint64_t seed, double* vel);
+
+/* ---- device context -------------------------------------------------- */
+/* p may be NULL: a list-only context (neighbor lists and rebuild checks, no
+ * force evaluation), for build_neighbor_list, which takes no parameters. */
+int tsf_create(const tsf_params* p, int device, tsf_ctx** out);
+void tsf_destroy(tsf_ctx* ctx);
+void* tsf_stream(tsf_ctx* ctx); /* the context's cudaStream_t */
+
+/* AtomSystem upload (system.hpp:14-27): positions, species, box.  Species ids
+ * must lie in [0, S).  Invalidates the neighbor list when n changes. */
+int tsf_set_system(tsf_ctx* ctx, int64_t n, const double* xyz, const int32_t* species,
+                   const double box[3], const uint8_t periodic[3]);
+int tsf_set_positions(tsf_ctx* ctx, const double* xyz);
+int tsf_get_positions(tsf_ctx* ctx, double* xyz);
+
+/* build_neighbor_list (neighbor.hpp:31, neighbor.cpp:37-132) on the device. */
+int tsf_build_neighbor_list(tsf_ctx* ctx, double cutoff, double skin);
+/* Adopt an externally built NeighborList (CSR offsets[n+1], neighbors). */
+int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* nbrs,
+                          double cutoff, double skin);
+/* needs_rebuild (neighbor.hpp:35, neighbor.cpp:134-141): *out = 0/1. */
+int tsf_needs_rebuild(tsf_ctx* ctx, int* out);
+/* Entry count of a list (TSF_LIST_SKIN or TSF_LIST_SHORT; the short list is
+ * refreshed from the current positions, as filter_all_segments does). */
+int64_t tsf_neighbor_entries(tsf_ctx* ctx, int which);
+int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbrs, int64_t cap);
+
+/* ---- force evaluation (evaluate_forces), precision fixed per symbol -----
+ * f64:   double compute, double accumulation          (PrecisionMode::OptD)
+ * mixed: float compute, double accumulation           (PrecisionMode::OptM)
+ * f32:   float compute, float per-atom accumulation    (PrecisionMode::OptS)
+ * Any of energy / forces (n*3) / virial (6: xx yy zz xy xz yz) may be NULL;
+ * results then stay on the device and the call does not synchronize. */
+int tsf_compute_f64(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
+int tsf_compute_mixed(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
+int tsf_compute_f32(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
+
+/* One-shot drop-in: upload positions (and species/box), build the list when
+ * it is missing or stale, evaluate, download.  precision: 0 f64, 1 mixed, 2 f32. */
+int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xyz,
+                        const int32_t* species, const double box[3], const uint8_t periodic[3],
+                        double skin, uint32_t flags, double* energy, double* forces,
+                        double* virial);
+
+/* Kernel launches issued by this context since creation (evidence counter). */
+int64_t tsf_launch_count(const tsf_ctx* ctx);
+
+/* Per-stage CUDA-event timing of every evaluation while enabled (adds one
+ * stream synchronization per evaluation).  ms[4] accumulates: filter, launch
+ * setup, main force kernel, overflow + reductions + scatter gather. */
+int tsf_profile_enable(tsf_ctx* ctx, int on);
+int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset);
+
+/* ---- GPU-resident velocity-Verlet NVE (engine.cpp:142-199) ------------- */
+int tsf_md_set_state(tsf_ctx* ctx, const double* vel, const double* masses /* S */);
+int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel);
+/* Runs `steps` steps; precision as above.  Thermo every thermo_every steps
+ * (and after the last): up to cap samples of (step, pe, ke) written to
+ * thermo[3*s..]; *nsamples receives the count; *rebuilds the rebuild count. */
+int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t flags,
+               int thermo_every, double* thermo, int64_t cap, int64_t* nsamples,
+               int64_t* rebuilds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TERSOFF_B200_H */

@@ -1,0 +1,585 @@
+// extern "C" boundary (include/tersoff_b200.h) over the device context.
+//
+// Error behaviour follows the reference: ConfigError / ParseError -> 2,
+// NumericError -> 3 (proj/include/tmd/error.hpp:9-21, tools/main.cpp:241-256);
+// CUDA failures -> 4.  Messages are kept per context and per thread.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tersoff_b200.h"
+#include "tsf_context.hpp"
+
+struct tsf_params {
+  tsf::Params p;
+};
+struct tsf_ctx {
+  tsf::Ctx c;
+};
+
+namespace tsf {
+
+// Host-side generators (tsf_generators.cpp).
+void diamond_lattice(int nx, int ny, int nz, double a0, std::int32_t sid, double* xyz,
+                     std::int32_t* species, double* box);
+void perturbed_lattice(const Params& p, int cells, double jitter, std::uint64_t seed,
+                       double* xyz, std::int32_t* species, double* masses, double* box);
+void maxwell_boltzmann(std::int64_t n, const std::int32_t* species, const double* masses,
+                       double temperature, std::uint64_t seed, double* v);
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(cudaGetErrorString(e)) + " (" + what + ")");
+}
+
+template <typename T>
+void DevBuf<T>::reserve(std::size_t n) {
+  if (n <= cap) return;
+  release();
+  TSF_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+  cap = n;
+}
+
+template <typename T>
+void DevBuf<T>::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+}
+
+template struct DevBuf<double>;
+template struct DevBuf<double4>;
+template struct DevBuf<int>;
+template struct DevBuf<unsigned char>;
+template struct DevBuf<unsigned long long>;
+template struct DevBuf<Row<double>>;
+template struct DevBuf<Row<float>>;
+
+void ensure_pinned(Ctx& c, std::size_t doubles) {
+  if (doubles <= c.pinned_cap) return;
+  if (c.pinned) cudaFreeHost(c.pinned);
+  c.pinned = nullptr;
+  c.pinned_cap = 0;
+  TSF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c.pinned), doubles * sizeof(double),
+                         cudaHostAllocDefault));
+  c.pinned_cap = doubles;
+}
+
+}  // namespace tsf
+
+namespace {
+
+using tsf::Ctx;
+constexpr int kMaxListSpecies = 1 << 20;  // list-only contexts accept any species id
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(Ctx* c, F&& f) {
+  int rc = TSF_OK;
+  try {
+    if (c) tsf::check_cuda(cudaSetDevice(c->device), "cudaSetDevice");
+    f();
+  } catch (const tsf::ConfigError& e) {
+    g_err = e.what();
+    rc = TSF_ERR_CONFIG;
+  } catch (const tsf::ParseError& e) {
+    g_err = e.what();
+    rc = TSF_ERR_CONFIG;
+  } catch (const tsf::NumericError& e) {
+    g_err = e.what();
+    rc = TSF_ERR_NUMERIC;
+  } catch (const tsf::CudaError& e) {
+    g_err = std::string("CUDA error: ") + e.what();
+    rc = TSF_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    rc = TSF_ERR_INTERNAL;
+  }
+  if (rc != TSF_OK && c) c->err = g_err;
+  return rc;
+}
+
+void check_species(const Ctx& c, std::int64_t n, const std::int32_t* species) {
+  const int s = c.has_potential ? c.params.species_count() : kMaxListSpecies;
+  for (std::int64_t a = 0; a < n; ++a)
+    if (species[a] < 0 || species[a] >= s)
+      throw tsf::ConfigError("atom " + std::to_string(a) + " has species id " +
+                             std::to_string(species[a]) + " but the parameter table defines " +
+                             std::to_string(s) + " species");
+}
+
+void upload_xyz(Ctx& c, const double* xyz) {
+  const std::size_t m = 3 * std::size_t(c.n);
+  if (m == 0) return;
+  tsf::ensure_pinned(c, m);
+  std::memcpy(c.pinned, xyz, m * sizeof(double));
+  TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), c.pinned, m * sizeof(double),
+                           cudaMemcpyHostToDevice, c.stream));
+  tsf::pack_positions(c);
+  c.forces_current = false;
+}
+
+void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* species,
+                const double* box, const std::uint8_t* per) {
+  if (n < 0 || n > (std::int64_t(1) << 30)) throw tsf::ConfigError("atom count out of range");
+  for (int ax = 0; ax < 3; ++ax)
+    if (!(box[ax] > 0.0)) throw tsf::ConfigError("simulation box edges must be positive");
+  check_species(c, n, species);
+  bool geometry_changed = n != c.n;
+  for (int ax = 0; ax < 3; ++ax) {
+    geometry_changed |= c.box.len[ax] != box[ax] || c.box.per[ax] != int(per[ax] != 0);
+    c.box.len[ax] = box[ax];
+    c.box.per[ax] = per[ax] != 0;
+  }
+  if (n != c.n) {
+    c.n = n;
+    c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
+    const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
+    c.pos.reserve(nn);
+    c.species.reserve(nn);
+    c.xyz_stage.reserve(3 * nn);
+    c.forces.reserve(3 * nn);
+    c.vel.reserve(3 * nn);
+    TSF_CUDA(cudaMemsetAsync(c.vel.get(), 0, 3 * nn * sizeof(double), c.stream));
+  }
+  if (geometry_changed) {
+    c.skin_list.valid = false;
+    c.short_list.valid = false;
+  }
+  if (n > 0)
+    TSF_CUDA(cudaMemcpy(c.species.get(), species, sizeof(int) * n, cudaMemcpyHostToDevice));
+  upload_xyz(c, xyz);
+}
+
+void download_forces(Ctx& c, double* forces) {
+  const std::size_t m = 3 * std::size_t(c.n);
+  if (m == 0) return;
+  tsf::ensure_pinned(c, m);
+  TSF_CUDA(cudaMemcpyAsync(c.pinned, c.forces.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
+                           c.stream));
+  TSF_CUDA(cudaStreamSynchronize(c.stream));
+  std::memcpy(forces, c.pinned, m * sizeof(double));
+}
+
+void raise_device_errors(Ctx& c) {
+  int f = 0;
+  TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  TSF_CUDA(cudaStreamSynchronize(c.stream));
+  if (f & tsf::kErrShortOverflow)
+    throw tsf::ConfigError("an atom has more than 32 neighbours within r_cut_max");
+  if (f & tsf::kErrNonFinite) throw tsf::NumericError("non-finite pair term");
+}
+
+void finish(Ctx& c, double* energy, double* forces, double* virial) {
+  if (!energy && !forces && !virial) return;
+  double res[8];
+  TSF_CUDA(cudaMemcpyAsync(res, c.result.get(), 7 * sizeof(double), cudaMemcpyDeviceToHost,
+                           c.stream));
+  if (forces) download_forces(c, forces);
+  raise_device_errors(c);
+  if (energy) *energy = res[0];
+  if (virial)
+    for (int q = 0; q < 6; ++q) virial[q] = res[1 + q];
+}
+
+void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
+  if (!c.has_potential)
+    throw tsf::ConfigError("context was created without a parameter table (list-only)");
+  if (!c.skin_list.valid)
+    throw tsf::ConfigError(
+        "no neighbor list: call tsf_build_neighbor_list or tsf_set_neighbor_list first");
+  c.mark(0);
+  tsf::list_filter(c, c.params.r_cut_max(), (flags & TSF_NO_FILTER) == 0);
+  c.mark(1);
+  tsf::compute(c, p, flags);
+  c.mark(4);
+  c.forces_current = true;
+  if (c.profile) {
+    TSF_CUDA(cudaEventSynchronize(c.ev[4]));
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0;
+      TSF_CUDA(cudaEventElapsedTime(&ms, c.ev[k], c.ev[k + 1]));
+      c.stage_ms[k] += ms;
+    }
+    ++c.profiled_calls;
+  }
+}
+
+int compute_entry(tsf_ctx* ctx, tsf::Precision p, std::uint32_t flags, double* e, double* f,
+                  double* w) {
+  return guard(&ctx->c, [&] {
+    evaluate(ctx->c, p, flags);
+    finish(ctx->c, e, f, w);
+  });
+}
+
+std::vector<int> download_ell(Ctx& c, const tsf::ListState& s, std::vector<int>& cnt) {
+  cnt.assign(std::size_t(c.n), 0);
+  std::vector<int> ell(std::size_t(s.cap) * c.npad);
+  if (c.n == 0) return ell;
+  TSF_CUDA(cudaMemcpyAsync(cnt.data(), s.cnt.get(), sizeof(int) * c.n, cudaMemcpyDeviceToHost,
+                           c.stream));
+  if (!ell.empty())
+    TSF_CUDA(cudaMemcpyAsync(ell.data(), s.nbr.get(), sizeof(int) * ell.size(),
+                             cudaMemcpyDeviceToHost, c.stream));
+  TSF_CUDA(cudaStreamSynchronize(c.stream));
+  return ell;
+}
+
+const tsf::ListState& list_for(Ctx& c, int which) {
+  if (!c.skin_list.valid) throw tsf::ConfigError("no neighbor list has been built");
+  if (which == TSF_LIST_SKIN) return c.skin_list;
+  if (which != TSF_LIST_SHORT) throw tsf::ConfigError("unknown list selector");
+  if (!c.has_potential) throw tsf::ConfigError("the short list needs a parameter table");
+  tsf::list_filter(c, c.params.r_cut_max(), true);
+  return c.short_list;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsf_error_message(void) { return g_err.c_str(); }
+const char* tsf_last_error(const tsf_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
+const char* tsf_version(void) { return "paper_1607_02904_b200 0.1.0 (sm_100a)"; }
+
+/* ---- parameters ---- */
+int tsf_params_parse(const char* text, size_t len, const char* source_name, tsf_params** out) {
+  return guard(nullptr, [&] {
+    *out = new tsf_params{tsf::parse_params(std::string_view(text, len),
+                                            source_name ? source_name : "<string>")};
+  });
+}
+int tsf_params_load(const char* path, tsf_params** out) {
+  return guard(nullptr, [&] { *out = new tsf_params{tsf::load_params(path)}; });
+}
+int tsf_params_builtin_silicon(tsf_params** out) {
+  return guard(nullptr, [&] { *out = new tsf_params{tsf::builtin_silicon()}; });
+}
+void tsf_params_free(tsf_params* p) { delete p; }
+int tsf_params_species_count(const tsf_params* p) { return p->p.species_count(); }
+const char* tsf_params_species_name(const tsf_params* p, int s) {
+  if (s < 0 || s >= p->p.species_count()) return nullptr;
+  return p->p.species()[std::size_t(s)].c_str();
+}
+int tsf_params_species_id(const tsf_params* p, const char* name) {
+  return p->p.species_id(name);
+}
+double tsf_params_r_cut_max(const tsf_params* p) { return p->p.r_cut_max(); }
+int tsf_params_flat_rows(const tsf_params* p, double* rows, size_t cap) {
+  const std::vector<double> r = p->p.flat_rows();
+  if (cap < r.size()) {
+    g_err = "row buffer too small";
+    return TSF_ERR_CONFIG;
+  }
+  std::copy(r.begin(), r.end(), rows);
+  return TSF_OK;
+}
+int64_t tsf_params_serialize(const tsf_params* p, char* buf, size_t cap) {
+  const std::string s = p->p.serialize();
+  if (buf && cap > 0) {
+    const std::size_t m = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), m);
+    buf[m] = '\0';
+  }
+  return int64_t(s.size());
+}
+
+/* ---- generators ---- */
+int64_t tsf_diamond_lattice_size(int nx, int ny, int nz) {
+  return int64_t(nx) * ny * nz * 8;
+}
+int tsf_make_diamond_lattice(int nx, int ny, int nz, double a0, int32_t species_id, double* xyz,
+                             int32_t* species, double* box) {
+  return guard(nullptr,
+               [&] { tsf::diamond_lattice(nx, ny, nz, a0, species_id, xyz, species, box); });
+}
+int tsf_perturbed_lattice(const tsf_params* p, int cells, double jitter, uint64_t seed,
+                          double* xyz, int32_t* species, double* masses, double* box) {
+  return guard(nullptr, [&] {
+    tsf::perturbed_lattice(p->p, cells, jitter, seed, xyz, species, masses, box);
+  });
+}
+int tsf_init_velocities(int64_t n, const int32_t* species, const double* masses,
+                        double temperature, uint64_t seed, double* vel) {
+  return guard(nullptr,
+               [&] { tsf::maxwell_boltzmann(n, species, masses, temperature, seed, vel); });
+}
+
+/* ---- context ---- */
+int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
+  *out = nullptr;
+  tsf_ctx* ctx = nullptr;
+  const int rc = guard(nullptr, [&] {
+    int count = 0;
+    tsf::check_cuda(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count)
+      throw tsf::ConfigError("CUDA device " + std::to_string(device) + " not available (" +
+                             std::to_string(count) + " visible)");
+    tsf::check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    ctx = new tsf_ctx{tsf::Ctx(p ? p->p : tsf::builtin_silicon())};
+    Ctx& c = ctx->c;
+    c.has_potential = p != nullptr;
+    c.device = device;
+    TSF_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.flags.reserve(8);
+    c.result.reserve(8);
+    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 8 * sizeof(int), c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.result.get(), 0, 8 * sizeof(double), c.stream));
+    tsf::upload_params(c);
+    c.masses.assign(std::size_t(c.params.species_count()), 28.0855);
+  });
+  if (rc != TSF_OK) {
+    if (ctx) tsf_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return TSF_OK;
+}
+
+void tsf_destroy(tsf_ctx* ctx) {
+  if (!ctx) return;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  if (c.pinned) cudaFreeHost(c.pinned);
+  c.pinned = nullptr;
+  for (auto& e : c.ev)
+    if (e) cudaEventDestroy(e);
+  cudaStream_t s = c.stream;
+  delete ctx;  // DevBufs free themselves
+  if (s) cudaStreamDestroy(s);
+}
+
+void* tsf_stream(tsf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+
+int tsf_profile_enable(tsf_ctx* ctx, int on) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (on && !c.ev[0])
+      for (auto& e : c.ev) TSF_CUDA(cudaEventCreate(&e));
+    c.profile = on != 0;
+  });
+}
+
+int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    for (int k = 0; k < 4; ++k) ms[k] = c.stage_ms[k];
+    if (calls) *calls = c.profiled_calls;
+    if (reset) {
+      for (double& v : c.stage_ms) v = 0;
+      c.profiled_calls = 0;
+    }
+  });
+}
+int64_t tsf_launch_count(const tsf_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int tsf_set_system(tsf_ctx* ctx, int64_t n, const double* xyz, const int32_t* species,
+                   const double box[3], const uint8_t periodic[3]) {
+  return guard(&ctx->c, [&] { set_system(ctx->c, n, xyz, species, box, periodic); });
+}
+int tsf_set_positions(tsf_ctx* ctx, const double* xyz) {
+  return guard(&ctx->c, [&] { upload_xyz(ctx->c, xyz); });
+}
+int tsf_get_positions(tsf_ctx* ctx, double* xyz) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    const std::size_t m = 3 * std::size_t(c.n);
+    if (m == 0) return;
+    tsf::unpack_positions(c);
+    tsf::ensure_pinned(c, m);
+    TSF_CUDA(cudaMemcpyAsync(c.pinned, c.xyz_stage.get(), m * sizeof(double),
+                             cudaMemcpyDeviceToHost, c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    std::memcpy(xyz, c.pinned, m * sizeof(double));
+  });
+}
+
+int tsf_build_neighbor_list(tsf_ctx* ctx, double cutoff, double skin) {
+  return guard(&ctx->c, [&] { tsf::list_build(ctx->c, cutoff, skin); });
+}
+
+int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* nbrs,
+                          double cutoff, double skin) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (offsets[0] != 0) throw tsf::ConfigError("neighbor offsets must start at 0");
+    int mx = 0;
+    for (std::int64_t a = 0; a < c.n; ++a) {
+      const int len = offsets[a + 1] - offsets[a];
+      if (len < 0) throw tsf::ConfigError("neighbor offsets must be non-decreasing");
+      mx = std::max(mx, len);
+    }
+    const int cap = std::max(4, (mx + 3) / 4 * 4);
+    std::vector<int> ell(std::size_t(cap) * c.npad, 0), cnt(std::size_t(c.npad), 0);
+    for (std::int64_t a = 0; a < c.n; ++a) {
+      cnt[std::size_t(a)] = offsets[a + 1] - offsets[a];
+      for (int s = offsets[a]; s < offsets[a + 1]; ++s) {
+        const int b = nbrs[s];
+        if (b < 0 || b >= c.n || b == a)
+          throw tsf::ConfigError("neighbor index out of range in segment of atom " +
+                                 std::to_string(a));
+        ell[std::size_t(s - offsets[a]) * c.npad + a] = b;
+      }
+    }
+    c.skin_list.cap = cap;
+    c.skin_list.nbr.reserve(ell.size());
+    c.skin_list.cnt.reserve(cnt.size());
+    TSF_CUDA(cudaMemcpy(c.skin_list.nbr.get(), ell.data(), sizeof(int) * ell.size(),
+                        cudaMemcpyHostToDevice));
+    TSF_CUDA(cudaMemcpy(c.skin_list.cnt.get(), cnt.data(), sizeof(int) * cnt.size(),
+                        cudaMemcpyHostToDevice));
+    c.skin_list.max_count = mx;
+    c.skin_list.valid = true;
+    c.cutoff = cutoff;
+    c.skin = skin;
+    c.short_max_stale = true;
+    tsf::snapshot_reference_positions(c);
+  });
+}
+
+int tsf_needs_rebuild(tsf_ctx* ctx, int* out) {
+  return guard(&ctx->c, [&] { *out = tsf::list_needs_rebuild(ctx->c) ? 1 : 0; });
+}
+
+int64_t tsf_neighbor_entries(tsf_ctx* ctx, int which) {
+  int64_t total = -1;
+  const int rc = guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    const tsf::ListState& s = list_for(c, which);
+    std::vector<int> cnt(std::size_t(c.n));
+    if (c.n > 0)
+      TSF_CUDA(cudaMemcpy(cnt.data(), s.cnt.get(), sizeof(int) * c.n, cudaMemcpyDeviceToHost));
+    total = 0;
+    for (int v : cnt) total += v;
+  });
+  return rc == TSF_OK ? total : -int64_t(rc);
+}
+
+int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbrs, int64_t cap) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    const tsf::ListState& s = list_for(c, which);
+    std::vector<int> cnt;
+    const std::vector<int> ell = download_ell(c, s, cnt);
+    std::int64_t w = 0;
+    offsets[0] = 0;
+    for (std::int64_t a = 0; a < c.n; ++a) {
+      for (int q = 0; q < cnt[std::size_t(a)]; ++q) {
+        if (w >= cap) throw tsf::ConfigError("neighbor export buffer too small");
+        nbrs[w++] = ell[std::size_t(q) * c.npad + a];
+      }
+      offsets[a + 1] = int32_t(w);
+    }
+  });
+}
+
+int tsf_compute_f64(tsf_ctx* ctx, uint32_t flags, double* e, double* f, double* w) {
+  return compute_entry(ctx, tsf::Precision::F64, flags, e, f, w);
+}
+int tsf_compute_mixed(tsf_ctx* ctx, uint32_t flags, double* e, double* f, double* w) {
+  return compute_entry(ctx, tsf::Precision::Mixed, flags, e, f, w);
+}
+int tsf_compute_f32(tsf_ctx* ctx, uint32_t flags, double* e, double* f, double* w) {
+  return compute_entry(ctx, tsf::Precision::F32, flags, e, f, w);
+}
+
+int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xyz,
+                        const int32_t* species, const double box[3], const uint8_t periodic[3],
+                        double skin, uint32_t flags, double* energy, double* forces,
+                        double* virial) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (precision < 0 || precision > 2) throw tsf::ConfigError("unknown precision selector");
+    set_system(c, n, xyz, species, box, periodic);
+    if (!c.skin_list.valid || c.skin != skin || c.cutoff != c.params.r_cut_max() ||
+        tsf::list_needs_rebuild(c))
+      tsf::list_build(c, c.params.r_cut_max(), skin);
+    evaluate(c, tsf::Precision(precision), flags);
+    finish(c, energy, forces, virial);
+  });
+}
+
+/* ---- MD ---- */
+int tsf_md_set_state(tsf_ctx* ctx, const double* vel, const double* masses) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    const int s = c.params.species_count();
+    for (int q = 0; q < s; ++q)
+      if (!(masses[q] > 0.0))
+        throw tsf::ConfigError("species " + std::to_string(q) + " has non-positive mass");
+    c.masses.assign(masses, masses + s);
+    const std::size_t m = 3 * std::size_t(c.n);
+    if (m == 0) return;
+    tsf::ensure_pinned(c, m);
+    std::memcpy(c.pinned, vel, m * sizeof(double));
+    TSF_CUDA(cudaMemcpyAsync(c.vel.get(), c.pinned, m * sizeof(double), cudaMemcpyHostToDevice,
+                             c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel) {
+  const int rc = xyz ? tsf_get_positions(ctx, xyz) : TSF_OK;
+  if (rc != TSF_OK || !vel) return rc;
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    const std::size_t m = 3 * std::size_t(c.n);
+    if (m == 0) return;
+    tsf::ensure_pinned(c, m);
+    TSF_CUDA(cudaMemcpyAsync(c.pinned, c.vel.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    std::memcpy(vel, c.pinned, m * sizeof(double));
+  });
+}
+
+int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t flags,
+               int thermo_every, double* thermo, int64_t cap, int64_t* nsamples,
+               int64_t* rebuilds) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (precision < 0 || precision > 2) throw tsf::ConfigError("unknown precision selector");
+    if (steps < 0) throw tsf::ConfigError("steps must be non-negative");
+    if (!(dt > 0.0)) throw tsf::ConfigError("dt must be positive");
+    if (thermo_every < 1) throw tsf::ConfigError("thermo interval must be at least 1");
+    if (!c.skin_list.valid)
+      throw tsf::ConfigError("no neighbor list: build one before running dynamics");
+    const tsf::Precision p = tsf::Precision(precision);
+    std::int64_t ns = 0, nreb = 0;
+    auto sample = [&](std::int64_t step) {
+      tsf::md_kinetic(c);
+      double res[8];
+      TSF_CUDA(cudaMemcpyAsync(res, c.result.get(), 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                               c.stream));
+      raise_device_errors(c);
+      if (thermo && ns < cap) {
+        thermo[3 * ns] = double(step);
+        thermo[3 * ns + 1] = res[0];
+        thermo[3 * ns + 2] = res[7];
+      }
+      ++ns;
+    };
+    if (!c.forces_current) evaluate(c, p, flags);
+    sample(0);
+    for (std::int64_t s = 1; s <= steps; ++s) {
+      tsf::md_kick(c, dt, true);
+      if (tsf::list_needs_rebuild(c)) {
+        tsf::list_build(c, c.cutoff, c.skin);
+        ++nreb;
+      }
+      evaluate(c, p, flags);
+      tsf::md_kick(c, dt, false);
+      if (s % thermo_every == 0 || s == steps) sample(s);
+    }
+    if (nsamples) *nsamples = ns;
+    if (rebuilds) *rebuilds = nreb;
+  });
+}
+
+}  // extern "C"

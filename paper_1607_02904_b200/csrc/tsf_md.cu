@@ -1,0 +1,137 @@
+// Position packing and the GPU-resident velocity-Verlet pieces
+// (proj/src/engine.cpp:142-166: half-kick, drift + wrap, ..., half-kick).
+#include "tsf_context.hpp"
+#include "tsf_units.hpp"
+
+namespace tsf {
+
+namespace {
+
+int blocks_for(std::int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
+
+__global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ species, int n,
+                       double4* __restrict__ pos) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  pos[a] = make_double4(xyz[3 * a], xyz[3 * a + 1], xyz[3 * a + 2], double(species[a]));
+}
+
+__global__ void k_unpack(const double4* __restrict__ pos, int n, double* __restrict__ xyz) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const double4 p = pos[a];
+  xyz[3 * a] = p.x;
+  xyz[3 * a + 1] = p.y;
+  xyz[3 * a + 2] = p.z;
+}
+
+// wrap_1d (box.hpp:41-46)
+__device__ __forceinline__ double wrap(double x, double len) {
+  x = __dsub_rn(x, __dmul_rn(len, floor(__ddiv_rn(x, len))));
+  if (x < 0.0) x = __dadd_rn(x, len);
+  if (x >= len) x = __dsub_rn(x, len);
+  return x;
+}
+
+struct Masses {
+  double m[kMaxSpecies];
+};
+
+__global__ void k_kick(double4* __restrict__ pos, double* __restrict__ vel,
+                       const double* __restrict__ f, int n, Masses ms, double dt, int drift,
+                       Box box) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  double4 p = pos[a];
+  const double k = __ddiv_rn(__dmul_rn(0.5, dt), __dmul_rn(ms.m[species_of(p)], kMvv2e));
+  double vx = __dadd_rn(vel[3 * a], __dmul_rn(f[3 * a], k));
+  double vy = __dadd_rn(vel[3 * a + 1], __dmul_rn(f[3 * a + 1], k));
+  double vz = __dadd_rn(vel[3 * a + 2], __dmul_rn(f[3 * a + 2], k));
+  vel[3 * a] = vx;
+  vel[3 * a + 1] = vy;
+  vel[3 * a + 2] = vz;
+  if (drift) {
+    p.x = __dadd_rn(p.x, __dmul_rn(vx, dt));
+    p.y = __dadd_rn(p.y, __dmul_rn(vy, dt));
+    p.z = __dadd_rn(p.z, __dmul_rn(vz, dt));
+    if (box.per[0]) p.x = wrap(p.x, box.len[0]);
+    if (box.per[1]) p.y = wrap(p.y, box.len[1]);
+    if (box.per[2]) p.z = wrap(p.z, box.len[2]);
+    pos[a] = p;
+  }
+}
+
+// Kinetic energy sum(0.5 m v^2 mvv2e) (system.cpp:16-21), block partials in a
+// fixed order then one block finishing the sum: deterministic.
+__global__ void __launch_bounds__(256) k_ke_partial(const double4* __restrict__ pos,
+                                                    const double* __restrict__ vel, int n,
+                                                    Masses ms, double* __restrict__ part) {
+  __shared__ double s[256];
+  double acc = 0;
+  for (int a = blockIdx.x * 256 + threadIdx.x; a < n; a += gridDim.x * 256) {
+    const double m = ms.m[species_of(pos[a])];
+    const double vx = vel[3 * a], vy = vel[3 * a + 1], vz = vel[3 * a + 2];
+    acc += 0.5 * m * (vx * vx + vy * vy + vz * vz) * kMvv2e;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void k_ke_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double s[256];
+  double acc = 0;
+  for (int b = threadIdx.x; b < nb; b += 256) acc += part[b];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+Masses masses_of(const Ctx& c) {
+  Masses m{};
+  for (std::size_t s = 0; s < c.masses.size() && s < std::size_t(kMaxSpecies); ++s)
+    m.m[s] = c.masses[s];
+  return m;
+}
+
+}  // namespace
+
+void pack_positions(Ctx& c) {
+  if (c.n == 0) return;
+  k_pack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.xyz_stage.get(), c.species.get(),
+                                                   int(c.n), c.pos.get());
+  ++c.launches;
+}
+
+void unpack_positions(Ctx& c) {
+  if (c.n == 0) return;
+  k_unpack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), int(c.n), c.xyz_stage.get());
+  ++c.launches;
+}
+
+void md_kick(Ctx& c, double dt, bool drift) {
+  if (c.n == 0) return;
+  k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), c.vel.get(), c.forces.get(),
+                                                   int(c.n), masses_of(c), dt, drift ? 1 : 0,
+                                                   c.box);
+  ++c.launches;
+}
+
+void md_kinetic(Ctx& c) {
+  constexpr int kParts = 296;
+  c.partials.reserve(std::size_t(kParts) * kRedWidth);
+  k_ke_partial<<<kParts, 256, 0, c.stream>>>(c.pos.get(), c.vel.get(), int(c.n), masses_of(c),
+                                             c.partials.get());
+  k_ke_final<<<1, 256, 0, c.stream>>>(c.partials.get(), kParts, c.result.get() + 7);
+  c.launches += 2;
+}
+
+}  // namespace tsf

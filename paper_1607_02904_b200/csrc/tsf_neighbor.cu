@@ -1,0 +1,358 @@
+// GPU cell-list neighbor build, the paper's cutoff filter (short list) and the
+// rebuild trigger.
+//
+// Output contract (bit-exact with the reference):
+//   build_neighbor_list  proj/src/neighbor.cpp:37-132  — full, symmetric list of
+//     every b != a with |min_image(x_b - x_a)|^2 <= (rc + skin)^2, computed with
+//     the reference's FP64 rounding sequence (no contraction), segments sorted
+//     ascending by atom index.  The cell grid is the reference's (same edge,
+//     same binning arithmetic, same deduplicated 27-stencil), so even ulp-level
+//     binning decisions at cell faces select the same candidate set.
+//   filter_all_segments  proj/src/neighbor.cpp:143-180 — skin entries with
+//     r^2 <= r_cut_max^2, order kept; verbatim copy when the filter is off.
+//   needs_rebuild        proj/src/neighbor.cpp:134-141 — any |dx|^2 > (skin/2)^2.
+//
+// Storage: ELL, column-major (nbr[s * npad + a]) + count[a].  One thread per
+// atom; at every slot s a warp touches 32 consecutive words.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "tsf_context.hpp"
+
+namespace tsf {
+
+namespace {
+
+struct Grid {
+  int nc[3];
+  double org[3], ext[3];
+};
+
+__device__ __forceinline__ int clamp_cell(double p, double org, double ext, int n) {
+  // int(floor(((p - o) / e) * n)) clamped to [0, n-1]  (neighbor.cpp:19-28)
+  const double f = __dmul_rn(__ddiv_rn(__dsub_rn(p, org), ext), double(n));
+  int c = int(floor(f));
+  return c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
+}
+
+__global__ void k_cell_count(const double4* __restrict__ pos, int n, Grid g,
+                             int* __restrict__ cell_of, int* __restrict__ count) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const double4 p = pos[a];
+  const int cx = clamp_cell(p.x, g.org[0], g.ext[0], g.nc[0]);
+  const int cy = clamp_cell(p.y, g.org[1], g.ext[1], g.nc[1]);
+  const int cz = clamp_cell(p.z, g.org[2], g.ext[2], g.nc[2]);
+  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx;
+  cell_of[a] = c;
+  atomicAdd(count + c, 1);
+}
+
+__global__ void k_cell_fill(int n, const int* __restrict__ cell_of,
+                            const int* __restrict__ start, int* __restrict__ fill,
+                            int* __restrict__ binned) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int c = cell_of[a];
+  binned[start[c] + atomicAdd(fill + c, 1)] = a;
+}
+
+// Unique wrapped neighbor coordinates along one axis (the per-axis factor of
+// the deduplicated 27-stencil, neighbor.cpp:84-103).
+__device__ __forceinline__ int axis_stencil(int c, int n, int per, int out[3]) {
+  int m = 0;
+  for (int d = -1; d <= 1; ++d) {
+    int w = c + d;
+    if (per) w = (w + n) % n;
+    if (w < 0 || w >= n) continue;
+    bool dup = false;
+    for (int q = 0; q < m; ++q) dup |= out[q] == w;
+    if (!dup) out[m++] = w;
+  }
+  return m;
+}
+
+template <int CAP>
+__global__ void __launch_bounds__(kBlock) k_skin_list(
+    const double4* __restrict__ pos, int n, int npad, Box box, Grid g, double bc2,
+    const int* __restrict__ cell_of, const int* __restrict__ start,
+    const int* __restrict__ binned, int cap, int* __restrict__ nbr, int* __restrict__ cnt,
+    int* __restrict__ max_count) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const double4 pa = pos[a];
+  const int home = cell_of[a];
+  const int cx = home % g.nc[0], cy = (home / g.nc[0]) % g.nc[1], cz = home / (g.nc[0] * g.nc[1]);
+  int sx[3], sy[3], sz[3];
+  const int mx = axis_stencil(cx, g.nc[0], box.per[0], sx);
+  const int my = axis_stencil(cy, g.nc[1], box.per[1], sy);
+  const int mz = axis_stencil(cz, g.nc[2], box.per[2], sz);
+  int buf[CAP];
+  int m = 0;
+  for (int iz = 0; iz < mz; ++iz)
+    for (int iy = 0; iy < my; ++iy)
+      for (int ix = 0; ix < mx; ++ix) {
+        const int c = (sz[iz] * g.nc[1] + sy[iy]) * g.nc[0] + sx[ix];
+        for (int t = start[c]; t < start[c + 1]; ++t) {
+          const int b = binned[t];
+          if (b == a) continue;
+          double dx, dy, dz;
+          displacement(pa, pos[b], box, dx, dy, dz);
+          if (norm_sq_exact(dx, dy, dz) <= bc2) {
+            if (m < CAP) buf[m] = b;
+            ++m;
+          }
+        }
+      }
+  atomicMax(max_count, m);
+  if (m > cap || m > CAP) return;  // host grows the capacity and rebuilds
+  // ascending atom index (neighbor.cpp:114)
+  for (int i = 1; i < m; ++i) {
+    const int v = buf[i];
+    int j = i - 1;
+    while (j >= 0 && buf[j] > v) {
+      buf[j + 1] = buf[j];
+      --j;
+    }
+    buf[j + 1] = v;
+  }
+  for (int s = 0; s < m; ++s) nbr[std::size_t(s) * npad + a] = buf[s];
+  cnt[a] = m;
+}
+
+// Short list: skin entries with r^2 <= r_cut_max^2 in segment order.
+__global__ void __launch_bounds__(kBlock) k_filter(
+    const double4* __restrict__ pos, int n, int npad, Box box, double rc2, int apply,
+    const int* __restrict__ skin, const int* __restrict__ skin_cnt, int* __restrict__ out,
+    int* __restrict__ out_cnt, int* __restrict__ max_count) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int m = skin_cnt[a];
+  int w = 0;
+  if (apply) {
+    const double4 pa = pos[a];
+    for (int s = 0; s < m; ++s) {
+      const int b = skin[std::size_t(s) * npad + a];
+      double dx, dy, dz;
+      displacement(pa, pos[b], box, dx, dy, dz);
+      if (norm_sq_exact(dx, dy, dz) <= rc2) out[std::size_t(w++) * npad + a] = b;
+    }
+  } else {
+    for (int s = 0; s < m; ++s) out[std::size_t(s) * npad + a] = skin[std::size_t(s) * npad + a];
+    w = m;
+  }
+  out_cnt[a] = w;
+  if (w > 0) atomicMax(max_count, w);
+}
+
+__global__ void k_needs_rebuild(const double4* __restrict__ pos,
+                                const double4* __restrict__ ref, int n, Box box,
+                                double limit_sq, int* __restrict__ flag) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  bool moved = false;
+  if (a < n) {
+    double dx, dy, dz;
+    displacement(ref[a], pos[a], box, dx, dy, dz);
+    moved = norm_sq_exact(dx, dy, dz) > limit_sq;
+  }
+  if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// Occupied extent of open axes (neighbor.cpp:50-77); order-preserving integer
+// keys let atomicMin/Max reduce doubles exactly.
+__device__ __forceinline__ unsigned long long ordered_key(double v) {
+  const unsigned long long b = __double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_extent(const double4* __restrict__ pos, int n,
+                         unsigned long long* __restrict__ mnmx) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const double4 p = pos[a];
+  const double v[3] = {p.x, p.y, p.z};
+  for (int ax = 0; ax < 3; ++ax) {
+    atomicMin(mnmx + ax, ordered_key(v[ax]));
+    atomicMax(mnmx + 3 + ax, ordered_key(v[ax]));
+  }
+}
+
+double from_key(unsigned long long k) {
+  const unsigned long long b = (k & 0x8000000000000000ull) ? (k & ~0x8000000000000000ull) : ~k;
+  double v;
+  std::memcpy(&v, &b, sizeof v);
+  return v;
+}
+
+int blocks_for(std::int64_t n) { return int((n + kBlock - 1) / kBlock); }
+
+template <int CAP>
+void launch_skin(Ctx& c, const Grid& g, double bc2, int cap) {
+  k_skin_list<CAP><<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+      c.pos.get(), int(c.n), c.npad, c.box, g, bc2, c.cell_of.get(), c.cell_start.get(),
+      c.binned.get(), cap, c.skin_list.nbr.get(), c.skin_list.cnt.get(), c.flags.get() + 3);
+  ++c.launches;
+}
+
+}  // namespace
+
+void list_build(Ctx& c, double cutoff, double skin) {
+  if (!(cutoff > 0.0)) throw ConfigError("neighbor cutoff must be positive");
+  if (skin < 0.0) throw ConfigError("neighbor skin must be non-negative");
+  for (int ax = 0; ax < 3; ++ax)
+    if (!(c.box.len[ax] > 0.0)) throw ConfigError("simulation box edges must be positive");
+  const double bc = cutoff + skin;
+  const double bc2 = bc * bc;
+  for (int ax = 0; ax < 3; ++ax)
+    if (c.box.per[ax] && c.box.len[ax] < 2.0 * bc)
+      throw ConfigError("periodic box edge " + std::to_string(c.box.len[ax]) +
+                        " A is below 2*(cutoff+skin) = " + std::to_string(2.0 * bc) +
+                        " A; minimum image would be ambiguous");
+  c.cutoff = cutoff;
+  c.skin = skin;
+  const int n = int(c.n);
+
+  // grid (neighbor.cpp:50-77)
+  double lo[3] = {0, 0, 0}, hi[3] = {c.box.len[0], c.box.len[1], c.box.len[2]};
+  if (!c.box.per[0] || !c.box.per[1] || !c.box.per[2]) {
+    DevBuf<unsigned long long> mm;
+    mm.reserve(6);
+    unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+    TSF_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+    if (n > 0) {
+      k_extent<<<blocks_for(n), kBlock, 0, c.stream>>>(c.pos.get(), n, mm.get());
+      ++c.launches;
+    }
+    unsigned long long got[6];
+    TSF_CUDA(cudaMemcpyAsync(got, mm.get(), sizeof got, cudaMemcpyDeviceToHost, c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    for (int ax = 0; ax < 3; ++ax) {
+      if (c.box.per[ax]) continue;
+      double mn = 0.0, mx = c.box.len[ax];
+      if (n > 0) {
+        mn = from_key(got[ax]);
+        mx = from_key(got[3 + ax]);
+      }
+      lo[ax] = mn;
+      hi[ax] = std::max(mx, mn + bc);
+    }
+  }
+  Grid g;
+  for (int ax = 0; ax < 3; ++ax) {
+    g.org[ax] = lo[ax];
+    g.ext[ax] = hi[ax] - lo[ax];
+    g.nc[ax] = std::max(1, int(std::floor(g.ext[ax] / bc)));
+  }
+  const std::int64_t ncells = std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2];
+  if (ncells > (1ll << 30)) throw ConfigError("cell grid too large");
+
+  c.cell_of.reserve(std::size_t(std::max(n, 1)));
+  c.binned.reserve(std::size_t(std::max(n, 1)));
+  c.cell_count.reserve(std::size_t(ncells) + 1);
+  c.cell_start.reserve(std::size_t(ncells) + 1);
+  c.cell_fill.reserve(std::size_t(ncells) + 1);
+  TSF_CUDA(cudaMemsetAsync(c.cell_count.get(), 0, sizeof(int) * (ncells + 1), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.cell_fill.get(), 0, sizeof(int) * (ncells + 1), c.stream));
+  if (n > 0) {
+    k_cell_count<<<blocks_for(n), kBlock, 0, c.stream>>>(c.pos.get(), n, g, c.cell_of.get(),
+                                                         c.cell_count.get());
+    ++c.launches;
+  }
+  std::size_t tmp = 0;
+  TSF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cell_count.get(), c.cell_start.get(),
+                                         int(ncells + 1), c.stream));
+  c.scan_tmp.reserve(tmp);
+  TSF_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.get(), tmp, c.cell_count.get(),
+                                         c.cell_start.get(), int(ncells + 1), c.stream));
+  ++c.launches;
+  if (n > 0) {
+    k_cell_fill<<<blocks_for(n), kBlock, 0, c.stream>>>(n, c.cell_of.get(), c.cell_start.get(),
+                                                        c.cell_fill.get(), c.binned.get());
+    ++c.launches;
+  }
+
+  int cap = c.skin_list.cap > 0 ? c.skin_list.cap : 32;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    c.skin_list.nbr.reserve(std::size_t(cap) * c.npad + 1);
+    c.skin_list.cnt.reserve(std::size_t(c.npad) + 1);
+    TSF_CUDA(cudaMemsetAsync(c.skin_list.cnt.get(), 0, sizeof(int) * c.npad, c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.flags.get() + 3, 0, sizeof(int), c.stream));
+    if (n > 0) {
+      if (cap <= 32) launch_skin<32>(c, g, bc2, cap);
+      else if (cap <= 64) launch_skin<64>(c, g, bc2, cap);
+      else if (cap <= 128) launch_skin<128>(c, g, bc2, cap);
+      else launch_skin<512>(c, g, bc2, cap);
+    }
+    int mx = 0;
+    TSF_CUDA(cudaMemcpyAsync(&mx, c.flags.get() + 3, sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    c.skin_list.max_count = mx;
+    if (mx <= cap) {
+      c.skin_list.cap = cap;
+      c.skin_list.valid = true;
+      break;
+    }
+    if (mx > 512)
+      throw ConfigError("more than 512 neighbors within cutoff+skin of one atom (" +
+                        std::to_string(mx) + ")");
+    cap = mx <= 32 ? 32 : mx <= 64 ? 64 : mx <= 128 ? 128 : 512;
+  }
+  snapshot_reference_positions(c);
+  c.short_max_stale = true;
+}
+
+void snapshot_reference_positions(Ctx& c) {
+  c.pos_ref.reserve(std::size_t(std::max<std::int64_t>(c.n, 1)));
+  TSF_CUDA(cudaMemcpyAsync(c.pos_ref.get(), c.pos.get(), sizeof(double4) * c.n,
+                           cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void list_filter(Ctx& c, double r_cut_max, bool apply) {
+  ListState& s = c.short_list;
+  s.cap = c.skin_list.cap;
+  s.nbr.reserve(std::size_t(s.cap) * c.npad + 1);
+  s.cnt.reserve(std::size_t(c.npad) + 1);
+  const bool reread = c.short_max_stale || c.short_apply != int(apply);
+  if (reread) TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
+  if (c.n > 0) {
+    k_filter<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+        c.pos.get(), int(c.n), c.npad, c.box, r_cut_max * r_cut_max, apply ? 1 : 0,
+        c.skin_list.nbr.get(), c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(),
+        c.flags.get() + 4);
+    ++c.launches;
+  }
+  s.valid = true;
+  if (reread) {
+    // Largest short count sizes the force kernel's lane group; read it back
+    // only after a rebuild — between rebuilds outgrown atoms take the
+    // overflow path, so the steady state never synchronizes here.
+    int mx = 0;
+    TSF_CUDA(cudaMemcpyAsync(&mx, c.flags.get() + 4, sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    s.max_count = mx;
+    c.short_max_stale = false;
+    c.short_apply = int(apply);
+  }
+}
+
+bool list_needs_rebuild(Ctx& c) {
+  if (!c.skin_list.valid) return true;
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 2, 0, sizeof(int), c.stream));
+  if (c.n > 0) {
+    k_needs_rebuild<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+        c.pos.get(), c.pos_ref.get(), int(c.n), c.box, 0.25 * c.skin * c.skin, c.flags.get() + 2);
+    ++c.launches;
+  }
+  int f = 0;
+  TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  TSF_CUDA(cudaStreamSynchronize(c.stream));
+  return f != 0;
+}
+
+}  // namespace tsf

@@ -1,0 +1,89 @@
+"""Seeded test systems shared by the CPU and GPU suites.
+
+Positions come from the product generators (bit-identical to the reference's
+make_diamond_lattice / perturbed_lattice, pinned in test_generators.py) or from
+numpy with a fixed seed; the same arrays feed the GPU path and the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Case:
+    name: str
+    xyz: np.ndarray
+    species: np.ndarray
+    box: np.ndarray
+    periodic: np.ndarray
+    skin: float
+    params_text: str
+
+
+def _wrap(xyz, box):
+    return np.mod(xyz, box)
+
+
+def si_text(tb):
+    return tb.builtin_silicon().serialize()
+
+
+def diamond(tb, cells=4, a0=5.431, skin=1.0, name=None):
+    s = tb.make_diamond_lattice(cells, cells, cells, a0)
+    return Case(name or f"diamond{cells}", s.positions, s.species, s.box.lengths,
+                s.box.periodic, skin, si_text(tb))
+
+
+def perturbed(tb, cells, jitter, seed, skin=0.5, text=None):
+    params = tb.builtin_silicon() if text is None else tb.parse_params(text)
+    s = tb.perturbed_lattice(params, cells, jitter, seed)
+    return Case(f"perturbed{cells}_{jitter}_{seed}", s.positions, s.species, s.box.lengths,
+                s.box.periodic, skin, params.serialize())
+
+
+def zincblende(tb, sic_text, cells=4, a0=4.32, jitter=0.0, seed=1, skin=1.0):
+    """3C-SiC: basis 0-3 Si, 4-7 C (SURVEY.md 8d cfg 3)."""
+    s = tb.make_diamond_lattice(cells, cells, cells, a0)
+    sp = np.where(np.arange(s.natoms) % 8 < 4, 0, 1).astype(np.int32)
+    xyz = s.positions.copy()
+    if jitter:
+        rng = np.random.default_rng(seed)
+        xyz = _wrap(xyz + rng.uniform(-jitter, jitter, xyz.shape), s.box.lengths)
+    return Case(f"sic{cells}_{jitter}", xyz, sp, s.box.lengths, s.box.periodic, skin, sic_text)
+
+
+def liquid_like(tb, cells=4, jitter=0.35, seed=5, skin=1.0):
+    """Strongly disordered Si: irregular short counts (3..8+) exercise the
+    group-width choice and the overflow path."""
+    s = tb.make_diamond_lattice(cells, cells, cells, 5.431)
+    rng = np.random.default_rng(seed)
+    xyz = _wrap(s.positions + rng.uniform(-jitter, jitter, s.positions.shape), s.box.lengths)
+    return Case(f"disordered{cells}_{jitter}", xyz, s.species, s.box.lengths, s.box.periodic,
+                skin, si_text(tb))
+
+
+def open_cluster(tb, n=64, seed=3, skin=0.5):
+    """Atoms in an open (non-periodic) box: occupied-extent binning path."""
+    s = tb.make_diamond_lattice(2, 2, 2, 5.431)
+    rng = np.random.default_rng(seed)
+    xyz = s.positions[:n] + 10.0 + rng.uniform(-0.1, 0.1, (n, 3))
+    return Case("open_cluster", xyz, s.species[:n], np.array([60.0, 60.0, 60.0]),
+                np.zeros(3, np.uint8), skin, si_text(tb))
+
+
+def dimer(tb, r=2.25):
+    xyz = np.array([[5.0, 5.0, 5.0], [5.0 + r, 5.0, 5.0]])
+    return Case("dimer", xyz, np.zeros(2, np.int32), np.array([60.0, 60.0, 60.0]),
+                np.zeros(3, np.uint8), 0.5, si_text(tb))
+
+
+def slab_mixed(tb):
+    """Periodic in x and y, open in z."""
+    s = tb.make_diamond_lattice(3, 3, 2, 5.431)
+    rng = np.random.default_rng(11)
+    xyz = s.positions + rng.uniform(-0.1, 0.1, s.positions.shape)
+    xyz[:, :2] = np.mod(xyz[:, :2], s.box.lengths[:2])
+    return Case("slab_xy", xyz, s.species, s.box.lengths, np.array([1, 1, 0], np.uint8), 0.8,
+                si_text(tb))

@@ -1,0 +1,280 @@
+"""GPU parity: libtersoff_b200.so against the CPU oracle on identical inputs.
+
+Bars (BASELINE.json north star):
+  neighbor lists and per-atom counts  bit-exact
+  double   energy rel <= 1e-12, forces abs <= 1e-10 eV/A
+  mixed / single  energy rel <= 1e-6, forces <= 1e-4 * max(1, max|F_ref|)
+Large-N energy is gated against the long-double oracle sum.
+"""
+import numpy as np
+import pytest
+
+import systems
+
+pytestmark = pytest.mark.gpu
+
+E_TOL_D, F_TOL_D = 1e-12, 1e-10
+E_TOL_M, F_TOL_M = 1e-6, 1e-4
+
+
+def _ctx(tb, case):
+    params = tb.parse_params(case.params_text)
+    ctx = tb.Context(params, 0)
+    ctx.set_system(case.xyz, case.species, case.box, case.periodic)
+    ctx.build_neighbor_list(params.r_cut_max, case.skin)
+    return params, ctx
+
+
+def _oracle(oracle, case, params):
+    from oracle.oracle import parse_param_text
+    op = parse_param_text(case.params_text)
+    off, nb = oracle.build_neighbor_list(case.xyz, case.box, case.periodic, op.r_cut_max,
+                                         case.skin)
+    ref = oracle.compute_ref(op, case.xyz, case.species, case.box, case.periodic, off, nb)
+    return op, off, nb, ref
+
+
+def _cases(tb, sic_text):
+    return [
+        systems.diamond(tb, 4),
+        systems.perturbed(tb, 4, 0.12, 32, skin=0.5),
+        systems.perturbed(tb, 2, 0.12, 722, skin=0.5),
+        systems.perturbed(tb, 2, 0.35, 41, skin=0.6),
+        systems.zincblende(tb, sic_text, 4, jitter=0.1, seed=1, skin=0.5),
+        systems.zincblende(tb, sic_text, 3, jitter=0.0, skin=1.0),
+        systems.liquid_like(tb, 4, 0.35, 5),
+        systems.open_cluster(tb),
+        systems.slab_mixed(tb),
+        systems.dimer(tb),
+    ]
+
+
+@pytest.fixture(scope="module")
+def cases(tb, sic_text):
+    return _cases(tb, sic_text)
+
+
+def test_neighbor_lists_bit_exact(tb, oracle, cases):
+    for case in cases:
+        params, ctx = _ctx(tb, case)
+        off, nb = ctx.export_neighbors("skin")
+        ooff, onb = oracle.build_neighbor_list(case.xyz, case.box, case.periodic,
+                                               params.r_cut_max, case.skin)
+        assert np.array_equal(off, ooff), case.name
+        assert np.array_equal(nb, onb), case.name
+        soff, snb = ctx.export_neighbors("short")
+        xoff, xnb = oracle.filter(case.xyz, case.box, case.periodic, ooff, onb, params.r_cut_max)
+        assert np.array_equal(soff, xoff), case.name
+        assert np.array_equal(snb, xnb), case.name
+        ctx.close()
+
+
+def test_neighbor_list_matches_brute_force(tb, oracle):
+    case = systems.perturbed(tb, 2, 0.35, 41, skin=0.6)
+    params, ctx = _ctx(tb, case)
+    off, nb = ctx.export_neighbors("skin")
+    boff, bnb = oracle.brute_neighbor_list(case.xyz, case.box, case.periodic,
+                                           params.r_cut_max + 0.6)
+    assert np.array_equal(off, boff) and np.array_equal(nb, bnb)
+
+
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_double_parity(tb, oracle, cases, deterministic):
+    for case in cases:
+        params, ctx = _ctx(tb, case)
+        _, _, _, ref = _oracle(oracle, case, params)
+        e, f, w = ctx.compute("double", deterministic=deterministic)
+        scale = abs(ref["energy"]) if ref["energy"] != 0 else 1.0
+        assert abs(e - ref["energy"]) <= E_TOL_D * scale, (case.name, e, ref["energy"])
+        assert np.abs(f - ref["forces"]).max(initial=0) <= F_TOL_D, case.name
+        wscale = max(1.0, np.abs(ref["virial"]).max())
+        assert np.abs(w - ref["virial"]).max() <= 1e-10 * wscale, (case.name, w, ref["virial"])
+        ctx.close()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "single"])
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_reduced_precision(tb, oracle, cases, precision, deterministic):
+    for case in cases:
+        params, ctx = _ctx(tb, case)
+        _, _, _, ref = _oracle(oracle, case, params)
+        e, f, w = ctx.compute(precision, deterministic=deterministic)
+        scale = abs(ref["energy"]) if ref["energy"] != 0 else 1.0
+        assert abs(e - ref["energy"]) <= E_TOL_M * scale, (case.name, e, ref["energy"])
+        fscale = max(1.0, np.abs(ref["forces"]).max(initial=0))
+        assert np.abs(f - ref["forces"]).max(initial=0) <= F_TOL_M * fscale, case.name
+        ctx.close()
+
+
+def test_appendix_d_goldens(tb):
+    """SURVEY.md Appendix D energies (bitwise reference outputs), double mode."""
+    params = tb.builtin_silicon()
+    for case, e_gold in [(systems.diamond(tb, 4), -2370.7709768772361),
+                         (systems.perturbed(tb, 4, 0.12, 32, 0.5), -2318.8092698921296),
+                         (systems.perturbed(tb, 2, 0.12, 722, 0.5), -289.24149471763792)]:
+        _, ctx = _ctx(tb, case)
+        e, f, _ = ctx.compute("double", deterministic=True)
+        assert abs(e - e_gold) <= 1e-12 * abs(e_gold)
+        ctx.close()
+    case = systems.perturbed(tb, 4, 0.12, 32, 0.5)
+    _, ctx = _ctx(tb, case)
+    _, f, _ = ctx.compute("double")
+    np.testing.assert_allclose(f[0], [-1.5906421510252808, -1.1016438175896053,
+                                      1.0033862477768203], rtol=0, atol=1e-10)
+
+
+def test_deterministic_mode_is_bitwise_reproducible(tb, sic_text):
+    for case in [systems.liquid_like(tb, 4, 0.35, 5), systems.zincblende(tb, sic_text, 4, jitter=0.1)]:
+        _, ctx = _ctx(tb, case)
+        for prec in ("double", "mixed", "single"):
+            e1, f1, w1 = ctx.compute(prec, deterministic=True)
+            e2, f2, w2 = ctx.compute(prec, deterministic=True)
+            assert e1 == e2 and np.array_equal(f1, f2) and np.array_equal(w1, w2)
+        ctx.close()
+
+
+def test_filter_off_matches_filter_on(tb, oracle):
+    """Acceptance criterion 5 (acceptance.cpp:195-230): 1e-12 relative."""
+    case = systems.perturbed(tb, 4, 0.12, 52, skin=0.5)
+    _, ctx = _ctx(tb, case)
+    e1, f1, _ = ctx.compute("double", deterministic=True, filter=True)
+    e2, f2, _ = ctx.compute("double", deterministic=True, filter=False)
+    scale = max(1.0, np.abs(f1).max())
+    assert abs(e1 - e2) <= 1e-12 * abs(e1)
+    assert np.abs(f1 - f2).max() <= 1e-12 * scale
+
+
+def test_overflow_path_between_rebuilds(tb, oracle):
+    """List built on an ordered lattice (4 short neighbours -> group width 4),
+    then atoms move inside the skin so some gain 5-8 short neighbours without
+    a rebuild: those atoms take the G = 32 overflow launch."""
+    base = systems.diamond(tb, 4, skin=1.0)
+    params, ctx = _ctx(tb, base)
+    rng = np.random.default_rng(9)
+    moved = np.mod(base.xyz + rng.uniform(-0.4, 0.4, base.xyz.shape), base.box)
+    ctx.set_positions(moved)
+    from oracle.oracle import parse_param_text
+    op = parse_param_text(base.params_text)
+    off, nb = ctx.export_neighbors("skin")          # the list built on `base`
+    soff, _ = ctx.export_neighbors("short")
+    assert np.diff(soff).max() > 4
+    ref = oracle.compute_ref(op, moved, base.species, base.box, base.periodic, off, nb)
+    for det in (True, False):
+        e, f, _ = ctx.compute("double", deterministic=det)
+        assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D
+
+
+def test_external_neighbor_list(tb, oracle):
+    """tsf_set_neighbor_list: evaluate on a list built elsewhere (the
+    reference's NeighborList), here the oracle's."""
+    case = systems.perturbed(tb, 3, 0.2, 7, skin=0.5)
+    params = tb.builtin_silicon()
+    op, off, nb, ref = _oracle(oracle, case, params)
+    ctx = tb.Context(params, 0)
+    ctx.set_system(case.xyz, case.species, case.box, case.periodic)
+    ctx.set_neighbor_list(off, nb, params.r_cut_max, case.skin)
+    e, f, _ = ctx.compute("double", deterministic=True)
+    assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+    assert np.abs(f - ref["forces"]).max() <= F_TOL_D
+
+
+def test_needs_rebuild_threshold(tb):
+    """test_neighbor.cpp:65-76: exactly skin/2 does not trigger, 0.51 skin does."""
+    xyz = np.array([[1.0, 1.0, 1.0], [3.0, 1.0, 1.0]])
+    box = np.array([60.0, 60.0, 60.0])
+    ctx = tb.Context(None, 0)
+    ctx.set_system(xyz, [0, 0], box, [0, 0, 0])
+    ctx.build_neighbor_list(2.5, 0.5)
+    assert not ctx.needs_rebuild()
+    x2 = xyz.copy()
+    x2[0, 0] = 0.75
+    ctx.set_positions(x2)
+    assert not ctx.needs_rebuild()
+    x2[0, 0] = 1.0 - 0.51 * 0.5
+    ctx.set_positions(x2)
+    assert ctx.needs_rebuild()
+
+
+def test_neighbor_boundary_inclusive(tb):
+    """test_neighbor.cpp:17-32: d = 3.5 with cutoff 3.0 + skin 0.5 is listed."""
+    for dist, listed in [(2.0, True), (3.5, True), (3.6, False)]:
+        ctx = tb.Context(None, 0)
+        ctx.set_system([[5, 5, 5], [5 + dist, 5, 5]], [0, 0], [60.0, 60.0, 60.0], [0, 0, 0])
+        ctx.build_neighbor_list(3.0, 0.5)
+        off, nb = ctx.export_neighbors("skin")
+        assert list(np.diff(off)) == ([1, 1] if listed else [0, 0])
+
+
+def test_bad_inputs_refused(tb):
+    params = tb.builtin_silicon()
+    case = systems.perturbed(tb, 2, 0.1, 3)
+    ctx = tb.Context(params, 0)
+    ctx.set_system(case.xyz, case.species, case.box, case.periodic)
+    with pytest.raises(tb.ConfigError):
+        ctx.build_neighbor_list(3.2, -0.1)
+    ctx.set_system(case.xyz, case.species, case.box * np.array([1, 0.6, 1]), case.periodic)
+    with pytest.raises(tb.ConfigError):
+        ctx.build_neighbor_list(3.2, 0.5)
+    with pytest.raises(tb.ConfigError):
+        ctx.set_system(case.xyz, np.full(len(case.xyz), 3, np.int32), case.box, case.periodic)
+    fresh = tb.Context(params, 0)
+    fresh.set_system(case.xyz, case.species, case.box, case.periodic)
+    with pytest.raises(tb.ConfigError):
+        fresh.compute("double")
+
+
+def test_trivial_systems(tb, oracle):
+    params = tb.builtin_silicon()
+    ctx = tb.Context(params, 0)
+    ctx.set_system(np.zeros((1, 3)) + 5.0, [0], [60.0, 60.0, 60.0], [0, 0, 0])
+    ctx.build_neighbor_list(params.r_cut_max, 0.5)
+    e, f, w = ctx.compute("double")
+    assert e == 0.0 and np.all(f == 0)
+    case = systems.dimer(tb, 2.25)
+    _, ctx = _ctx(tb, case)
+    e, f, _ = ctx.compute("double", deterministic=True)
+    ref = _oracle(oracle, case, params)[3]
+    assert abs(e - ref["energy"]) <= 1e-14 * abs(ref["energy"])
+    assert f[0, 1] == 0 and f[0, 2] == 0 and abs(f[0, 0] + f[1, 0]) <= 1e-15
+
+
+def test_evaluate_forces_api(tb, oracle):
+    """The tersoffmd-shaped surface: options validated like potential_opt.cpp."""
+    params = tb.builtin_silicon()
+    s = tb.perturbed_lattice(params, 2, 0.12, 722)
+    lst = tb.build_neighbor_list(s, params.r_cut_max, 0.5)
+    assert lst.natoms == 64 and lst.pair_count == 312
+    assert not tb.needs_rebuild(lst, s)
+    e, f = tb.evaluate_forces(s, lst, params)
+    assert abs(e - (-289.24149471763792)) <= 1e-12 * 289.3
+    assert np.abs(f.sum(axis=0)).max() < 1e-10
+    e8, f8 = tb.evaluate_forces(s, lst, params, scheme="v2", width=8, deterministic=False)
+    assert abs(e8 - e) <= 1e-12 * abs(e) and np.abs(f8 - f).max() <= 1e-10
+    es, _ = tb.evaluate_forces(s, lst, params, precision="single")
+    assert abs(es - e) <= 1e-6 * abs(e)
+    with pytest.raises(tb.ConfigError):
+        tb.evaluate_forces(s, lst, params, scheme="v9")
+    with pytest.raises(tb.ConfigError):
+        tb.evaluate_forces(s, lst, params, width=3)
+    with pytest.raises(tb.ConfigError):
+        tb.evaluate_forces(s, lst, params, scheme="ref", precision="single")
+
+
+def test_large_n_against_compensated_oracle(tb, oracle):
+    """32k atoms (cfg-2 size): energy vs the long-double oracle sum."""
+    s = tb.make_diamond_lattice(20, 20, 10)
+    rng = np.random.default_rng(2)
+    xyz = np.mod(s.positions + rng.uniform(-0.1, 0.1, s.positions.shape), s.box.lengths)
+    case = systems.Case("si32k", xyz, s.species, s.box.lengths, s.box.periodic, 1.0,
+                        systems.si_text(tb))
+    params, ctx = _ctx(tb, case)
+    _, _, _, ref = _oracle(oracle, case, params)
+    for det in (True, False):
+        e, f, _ = ctx.compute("double", deterministic=det)
+        assert abs(e - ref["energy_ld"]) <= 1e-12 * abs(ref["energy_ld"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D
+    for prec in ("mixed", "single"):
+        e, f, _ = ctx.compute(prec)
+        assert abs(e - ref["energy_ld"]) <= E_TOL_M * abs(ref["energy_ld"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_M * max(1, np.abs(ref["forces"]).max())
