@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Tersoff force path (BASELINE.json metric: Tersoff
+atom-steps/s on Si).
+
+One step = one full evaluation of the hot path over the resident system:
+short-list filter (paper Sec. 4.4) + fused zeta / bond-order / force kernel +
+energy and virial reduction (+ deterministic gather when --deterministic).
+The neighbor list is built once before timing, as a current list between
+rebuilds (every ~25 steps at 1600 K).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision double|mixed|single]
+                  [--config si2m|si32k|sic256k] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  `value` is device-resident throughput (CUDA
+events on the context's stream, max over ranks); `e2e` is the same metric
+through the reference-facing C-ABI call tsf_evaluate_forces with host
+buffers (positions H2D and forces/energy/virial D2H inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Tersoff atom-steps/s (Si 32k/2M atoms)"
+UNIT = "atom-steps/s"
+
+CONFIGS = {
+    # name: (cells, a0, jitter, params, description)
+    "si2m": ((80, 80, 40), 5.431, 0.15, "si",
+             "BASELINE cfg 4: Si diamond 80x80x40 = 2,048,000 atoms"),
+    "si32k": ((20, 20, 10), 5.431, 0.15, "si", "BASELINE cfg 2 size: Si diamond 20x20x10 = 32,000 atoms"),
+    "sic256k": ((32, 32, 32), 4.32, 0.10, "sic",
+                "BASELINE cfg 3: 3C-SiC zincblende 32^3 = 262,144 atoms"),
+}
+DTYPES = {"double": "f64", "mixed": "f32 compute / f64 accumulate", "single": "f32"}
+REF_OPTS = {"double": ("v1", "opt-d", 4), "mixed": ("v2", "opt-m", 8),
+            "single": ("v2", "opt-s", 8)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def make_system(cfg: str):
+    """Synthetic input of the workload: diamond (or zincblende) lattice with a
+    seeded uniform thermal-like jitter (positions wrapped into the box)."""
+    import paper_1607_02904_b200 as tb
+    cells, a0, jitter, pkind, _ = CONFIGS[cfg]
+    s = tb.make_diamond_lattice(*cells, a0)
+    rng = np.random.default_rng(12345)
+    xyz = np.mod(s.positions + rng.uniform(-jitter, jitter, s.positions.shape), s.box.lengths)
+    if pkind == "sic":
+        text = open(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")).read()
+        species = np.where(np.arange(s.natoms) % 8 < 4, 0, 1).astype(np.int32)
+        masses = [28.0855, 12.011]
+    else:
+        text = tb.builtin_silicon().serialize()
+        species = s.species
+        masses = [28.0855]
+    return text, np.ascontiguousarray(xyz), species, s.box.lengths, s.box.periodic, masses
+
+
+def algorithmic_work(xyz, species, box, offsets, nbrs, rows, ns):
+    """P pairs inside their (si,sj,sj) cutoff and T triplets inside (si,sj,sk),
+    on the short list, as the reference counts them:
+    ALGO_FLOP = 75 P + 143 T, ALGO_TRANSC = 8 P + 4 T."""
+    cnt = np.diff(offsets)
+    i = np.repeat(np.arange(len(cnt)), cnt)
+    d = xyz[nbrs] - xyz[i]
+    d -= box * np.floor(d / box + 0.5)
+    r2 = np.einsum("ij,ij->i", d, d)
+    si, sj = species[i], species[nbrs]
+    cutsq = rows[:, 15]
+    pair_ok = r2 <= cutsq[(si * ns + sj) * ns + sj]
+    P = int(pair_ok.sum())
+    if ns == 1 and pair_ok.all():
+        T = int(np.sum(cnt * (cnt - 1)))
+    else:
+        T = 0
+        starts = offsets[:-1]
+        for slot_j in range(int(cnt.max(initial=0))):
+            has_j = cnt > slot_j
+            ej = starts[has_j] + slot_j
+            for slot_k in range(int(cnt.max(initial=0))):
+                if slot_k == slot_j:
+                    continue
+                m = has_j & (cnt > slot_k)
+                ej2 = starts[m] + slot_j
+                ek = starts[m] + slot_k
+                okj = pair_ok[ej2]
+                row = (si[ej2] * ns + sj[ej2]) * ns + sj[ek]
+                T += int(np.sum(okj & (r2[ek] <= cutsq[row])))
+            del ej
+    return P, T
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), r[3:]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def load_peak(precision: str):
+    path = os.path.join(ROOT, "profiles", "fp_peaks_b200.json")
+    if os.path.exists(path):
+        pk = json.load(open(path))
+        key = "fp64_tflops" if precision == "double" else "fp32_tflops"
+        return pk[key], f"measured ({os.path.relpath(path, ROOT)}: {key})"
+    return (37.2 if precision == "double" else 74.4), "derived (148 SM x 1.965 GHz x FMA lanes)"
+
+
+def load_traffic(cfg: str, precision: str, det: bool):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    tab = json.load(open(path))
+    return tab.get(f"{cfg}/{precision}/{'det' if det else 'atomic'}")
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref = unmodified /root/reference sources), all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Reference, reference_available
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libtmdref.so not built (run __graft_entry__.build())"}))
+        return
+    R = Reference()
+    text, xyz, species, box, per, masses = make_system(args.config)
+    n = len(xyz)
+    ph = R.params(text)
+    sh = R.system(xyz, species, masses, box, per)
+    lh = R.neighbor_list(sh, R.lib.tmdref_params_r_cut_max(ph), 1.0)
+    scheme, prec, width = REF_OPTS[args.precision]
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        R.evaluate(sh, lh, ph, n, scheme, prec, width, 16, cores, True, with_forces=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        R.evaluate(sh, lh, ph, n, scheme, prec, width, 16, cores, True, with_forces=False)
+    t = time.perf_counter() - t0
+    value = n * args.steps / t
+    sample = (f"evaluate_forces({scheme}, width {width}, {prec}, workers={cores}) on the full "
+              f"{n}-atom system per step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": DTYPES[args.precision], "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][4], "precision": args.precision},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline(text, xyz, species, box, per, masses):
+    """compute_ref (paper Alg. 2, 1 thread) of the unmodified reference on the
+    same system: one call (~10 s at 2M atoms)."""
+    from oracle.oracle import Reference, reference_available
+    if not reference_available():
+        return None
+    R = Reference()
+    n = len(xyz)
+    ph = R.params(text)
+    sh = R.system(xyz, species, masses, box, per)
+    lh = R.neighbor_list(sh, R.lib.tmdref_params_r_cut_max(ph), 1.0)
+    t0 = time.perf_counter()
+    R.compute_ref(sh, lh, ph, n, with_forces=False)
+    t = time.perf_counter() - t0
+    return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"compute_ref (1 thread) on the full {n}-atom system, one call, {t:.2f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--precision", default="double", choices=list(DTYPES))
+    ap.add_argument("--config", default="si2m", choices=list(CONFIGS))
+    ap.add_argument("--deterministic", action="store_true")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_1607_02904_b200 as tb
+    from paper_1607_02904_b200 import _lib as L
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+
+    text, xyz, species, box, per, masses = make_system(args.config)
+    n = len(xyz)
+    params = tb.parse_params(text)
+    ctx = tb.Context(params, local)
+    ctx.set_system(xyz, species, box, per)
+    ctx.build_neighbor_list(params.r_cut_max, 1.0)
+    soff, snb = ctx.export_neighbors("short")
+    P, T = algorithmic_work(xyz, species, box, soff, snb, params.rows, params.species_count)
+    algo_flop = 75 * P + 143 * T
+
+    stream = torch.cuda.ExternalStream(ctx.stream, device=local)
+    def step():
+        ctx.compute(args.precision, deterministic=args.deterministic, energy=False,
+                    forces=False, virial=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    clocks = ClockSampler(local)
+    l0 = ctx.launches
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launches - l0
+    t = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    value = n * world * args.steps / t      # replicas: every rank evaluates the full system
+
+    # per-stage timing pass (separate from the timed region)
+    ctx.profile(True)
+    for _ in range(args.steps):
+        step()
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(False)
+    calls = max(prof["calls"], 1)
+    force_s = prof["force_ms"] / calls / 1e3
+    stage_total = prof["filter_ms"] + prof["setup_ms"] + prof["force_ms"] + prof["tail_ms"]
+    peak, peak_src = load_peak(args.precision)
+    achieved = algo_flop / force_s / 1e12
+
+    # e2e through the drop-in C-ABI call with host buffers
+    e2e = None
+    if not args.no_e2e:
+        lib = L.lib()
+        hx = torch.from_numpy(xyz.copy()).pin_memory()
+        hf = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        sp = np.ascontiguousarray(species, np.int32)
+        bx = np.ascontiguousarray(box, np.float64)
+        pr = np.ascontiguousarray(per, np.uint8)
+        energy = C.c_double()
+        vir = np.zeros(6)
+        pcode = {"double": 0, "mixed": 1, "single": 2}[args.precision]
+        flags = L.TSF_DETERMINISTIC if args.deterministic else 0
+
+        def call():
+            rc = lib.tsf_evaluate_forces(ctx._h, pcode, n, C.c_void_p(hx.data_ptr()),
+                                         sp.ctypes.data_as(C.c_void_p),
+                                         bx.ctypes.data_as(C.c_void_p),
+                                         pr.ctypes.data_as(C.c_void_p), 1.0, flags,
+                                         C.byref(energy), C.c_void_p(hf.data_ptr()),
+                                         vir.ctypes.data_as(C.c_void_p))
+            if rc:
+                raise RuntimeError(lib.tsf_last_error(ctx._h).decode())
+        for _ in range(args.warmup):
+            call()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            call()
+        e1.record(stream)
+        e1.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            tt = torch.tensor([te], device=f"cuda:{local}")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": n * world * args.steps / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(hx.numel() * 8),
+               "d2h_bytes_per_step": int(hf.numel() * 8 + 8 + 48),
+               "ms_per_step": 1e3 * te / args.steps,
+               "call": "tsf_evaluate_forces (include/tersoff_b200.h), pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(text, xyz, species, box, per, masses)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": DTYPES[args.precision], "data": "synthetic",
+            "config": {
+                "workload": CONFIGS[args.config][4] + ", seeded uniform +-%.2f A jitter, skin "
+                            "1.0 A; one filter + force/energy/virial evaluation per step"
+                            % CONFIGS[args.config][2],
+                "n_atoms": n, "precision": args.precision,
+                "scatter": "deterministic gather" if args.deterministic else "atomics",
+                "parallelism": "replicas" if world > 1 else "single GPU",
+                "l2": "inputs larger than L2 (positions + lists + forces > 126 MB at 2M atoms)"
+                      if n >= 1_000_000 else "inputs fit in L2",
+            },
+            "roofline": {
+                "bound": "fp64" if args.precision == "double" else "fp32",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.config, args.precision,
+                                                                 args.deterministic),
+                "kernel": "k_force (main launch)", "peak_source": peak_src,
+                "algo_flop_per_launch": algo_flop, "pairs": P, "triplets": T,
+                "algo_flop_formula": "75 P + 143 T (SURVEY.md 8d / Appendix A)",
+                "kernel_ms": force_s * 1e3,
+                "stage_ms_per_step": {k: prof[k] / calls for k in
+                                      ("filter_ms", "setup_ms", "force_ms", "tail_ms")},
+                "force_share_of_step": prof["force_ms"] / stage_total if stage_total else None,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

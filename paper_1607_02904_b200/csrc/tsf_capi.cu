@@ -112,13 +112,28 @@ void check_species(const Ctx& c, std::int64_t n, const std::int32_t* species) {
                              std::to_string(s) + " species");
 }
 
+// Page-locked caller buffers go straight over PCIe; pageable ones through the
+// context's pinned staging buffer.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
 void upload_xyz(Ctx& c, const double* xyz) {
   const std::size_t m = 3 * std::size_t(c.n);
   if (m == 0) return;
-  tsf::ensure_pinned(c, m);
-  std::memcpy(c.pinned, xyz, m * sizeof(double));
-  TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), c.pinned, m * sizeof(double),
-                           cudaMemcpyHostToDevice, c.stream));
+  const double* src = xyz;
+  if (!is_pinned(xyz)) {
+    tsf::ensure_pinned(c, m);
+    std::memcpy(c.pinned, xyz, m * sizeof(double));
+    src = c.pinned;
+  }
+  TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), src, m * sizeof(double), cudaMemcpyHostToDevice,
+                           c.stream));
   tsf::pack_positions(c);
   c.forces_current = false;
 }
@@ -150,14 +165,26 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.skin_list.valid = false;
     c.short_list.valid = false;
   }
-  if (n > 0)
-    TSF_CUDA(cudaMemcpy(c.species.get(), species, sizeof(int) * n, cudaMemcpyHostToDevice));
+  // species change rarely: re-upload only when they differ from the last upload
+  if (n > 0 && (c.host_species.size() != std::size_t(n) ||
+                std::memcmp(c.host_species.data(), species, sizeof(int) * n) != 0)) {
+    c.host_species.assign(species, species + n);
+    TSF_CUDA(cudaMemcpyAsync(c.species.get(), c.host_species.data(), sizeof(int) * n,
+                             cudaMemcpyHostToDevice, c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+  }
   upload_xyz(c, xyz);
 }
 
 void download_forces(Ctx& c, double* forces) {
   const std::size_t m = 3 * std::size_t(c.n);
   if (m == 0) return;
+  if (is_pinned(forces)) {
+    TSF_CUDA(cudaMemcpyAsync(forces, c.forces.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
   tsf::ensure_pinned(c, m);
   TSF_CUDA(cudaMemcpyAsync(c.pinned, c.forces.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
                            c.stream));

@@ -62,6 +62,7 @@ struct Ctx {
   int npad = 0;
   Box box{};
   DevBuf<int> species;         // [n]
+  std::vector<int> host_species;  // last uploaded species ids
   DevBuf<double4> pos;         // {x, y, z, species}
   DevBuf<double4> pos_ref;     // positions at the last list build (needs_rebuild)
   DevBuf<double> xyz_stage;    // AoS staging for H2D / D2H
