@@ -49,6 +49,7 @@ struct Ctx {
   Params params;
   bool has_potential = true;   // false: list-only context (tsf_create with NULL params)
   bool hoist_ramp = true;
+  bool fuse_filter = true;     // filter inside the force kernel (env TSF_FUSE_FILTER=0: separate)
   std::string err;
   std::int64_t launches = 0;
 

@@ -1,0 +1,707 @@
+// Tersoff energy / forces / virial on the short list — the hot path.
+//
+// Replaces evaluate_forces' kernels (proj/include/tmd/kernels.hpp:175-494,
+// proj/src/potential_ref.cpp:75-134; paper Alg. 2/3 and Fig. 3).
+//
+// Mapping ("lane group per atom", the GPU form of the paper's scheme (a)):
+//   * a group of G lanes (G = 4, 8, 16 or 32; G >= the atom's short count)
+//     owns central atom i; lane l holds short neighbour j_l, its FP64
+//     displacement (the reference's exact rounding, so the cutoff decisions are
+//     the reference's), r, 1/r, unit vector and f_C(r), f_C'(r), staged in
+//     shared memory as 128-bit vectors;
+//   * zeta pass: at rotation t lane l pairs with k = slot (l + t) mod n_i
+//     (t = 1..n_i-1 visits every k != j once); the triplet's d zeta/d x_j is
+//     accumulated in registers and d zeta/d x_k cached in registers (Alg. 3's
+//     derivative cache with k_max = G - 1; recomputed for G > 8);
+//   * pair block: V, dV/dr, dV/dzeta with the log-space bond order;
+//   * scatter pass: at rotation t lane l hands its cached d zeta/d x_k times
+//     dV/dzeta_j to lane (l + t) mod n_i with one shuffle — the transposed
+//     reduction — so every lane ends with P_l, the total force atom i's terms
+//     put on neighbour j_l, and F_i = -sum_l P_l (translation invariance);
+//   * atomic mode: one atomicAdd per neighbour slot and component, one for i;
+//     deterministic mode: P_l goes to a slot buffer and k_gather sums every
+//     atom's incoming slots in list order — bitwise reproducible;
+//   * energy and virial (W_ab = sum_l d_a P_b) are reduced per block into a
+//     partials array and summed in fixed order: deterministic in both modes.
+// The grid is persistent (a few blocks per SM striding over atom tiles): one
+// parameter load and one block reduction per block.  Atoms whose short count
+// exceeds G are queued and processed by the same code with G = 32 (one warp
+// per atom) in a second launch that exits at once when the queue is empty.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include "tsf_context.hpp"
+
+namespace tsf {
+
+namespace {
+
+template <typename R>
+struct ForceArgs {
+  Row<R> row0;         // single-species row: read straight from the constant bank
+  double cut0;
+  const double4* pos;
+  int n_owned;
+  int npad;
+  Box box;
+  const int* nbr;      // short list (unfused) or output short list (fused)
+  const int* cnt;
+  const int* skin;     // fused filter: skin list input
+  const int* skin_cnt;
+  int* short_out;      // fused filter: short list written as a by-product
+  int* short_cnt_out;
+  double rc2;          // r_cut_max^2 of the filter (neighbor.cpp:143-152)
+  const void* rows;
+  const double* cutsq;
+  int ns;
+  void* forces;        // atomic mode: Acc[n][3]
+  void* slot_x;        // deterministic mode: Acc[cap * npad] per component
+  void* slot_y;
+  void* slot_z;
+  void* fself;         // deterministic mode: Acc[n][3]
+  double* partials;    // [blocks][kRedWidth]
+  int partial_base;
+  int* overflow;       // queued atom ids
+  int* flags;          // [0] error bits, [1] overflow count
+};
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Parameter-table specialisations.
+enum Spec : int {
+  kSingle = 0,   // one species: the row lives in registers
+  kHoist = 1,    // several species, ramp (R, D) depends on (i, k) only
+  kGeneric = 2,  // anything else: ramp and cutoff test per triplet
+};
+
+template <typename R>
+struct Nbr {
+  R ux, uy, uz, r, ir;
+};
+
+template <typename R>
+struct Grad {
+  R z, jx, jy, jz, kx, ky, kz;
+};
+
+// Per-lane neighbour record in shared memory, 128-bit vectors.
+template <typename R> struct Stage;
+template <> struct Stage<double> {
+  double2 a[kBlock];   // ux, uy
+  double2 b[kBlock];   // uz, r
+  double2 c[kBlock];   // 1/r, fc
+  double2 d[kBlock];   // fc', meta (species, -1 when not a usable k)
+  __device__ void put(int t, const Nbr<double>& n, double fc, double dfc, int meta) {
+    a[t] = make_double2(n.ux, n.uy);
+    b[t] = make_double2(n.uz, n.r);
+    c[t] = make_double2(n.ir, fc);
+    d[t] = make_double2(dfc, double(meta));
+  }
+  __device__ void get(int t, Nbr<double>& n, double& fc, double& dfc, double& meta) const {
+    const double2 va = a[t], vb = b[t], vc = c[t], vd = d[t];
+    n.ux = va.x; n.uy = va.y; n.uz = vb.x; n.r = vb.y; n.ir = vc.x;
+    fc = vc.y; dfc = vd.x; meta = vd.y;
+  }
+};
+template <> struct Stage<float> {
+  float4 a[kBlock];    // ux, uy, uz, r
+  float4 b[kBlock];    // 1/r, fc, fc', meta
+  __device__ void put(int t, const Nbr<float>& n, float fc, float dfc, int meta) {
+    a[t] = make_float4(n.ux, n.uy, n.uz, n.r);
+    b[t] = make_float4(n.ir, fc, dfc, float(meta));
+  }
+  __device__ void get(int t, Nbr<float>& n, float& fc, float& dfc, float& meta) const {
+    const float4 va = a[t], vb = b[t];
+    n.ux = va.x; n.uy = va.y; n.uz = va.z; n.r = va.w; n.ir = vb.x;
+    fc = vb.y; dfc = vb.z; meta = vb.w;
+  }
+};
+
+// One (i, j, k) triplet: zeta term and its j and k gradients
+// (potential.hpp:132-198; the i gradient is never formed: F_i = -sum P).
+template <typename R>
+__device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R fck, R dfck,
+                                           const Row<R>& p) {
+  Grad<R> o;
+  R cs = j.ux * k.ux + j.uy * k.uy + j.uz * k.uz;
+  cs = fmin(R(1), fmax(R(-1), cs));
+  const R t = p.h - cs;
+  const R den = p.d2 + t * t;
+  const R iden = R(1) / den;
+  const R g = p.gamma + p.gcd2 * (t * t) * iden;
+  const R dg = R(-2) * p.gc2 * t * iden * iden;
+  const R arg = p.lam3 * (j.r - k.r);
+  const bool cubic = p.m3 != R(0);
+  const R ex = Fn<R>::exp_(cubic ? arg * arg * arg : arg);
+  const R dex = ex * p.lam3 * (cubic ? R(3) * arg * arg : R(1));
+  const R fg = fck * g;
+  o.z = fg * ex;
+  const R fgd = fck * dg * ex;
+  const R fge = fg * dex;
+  const R cge = dfck * g * ex;
+  // d cos / d x_j and d cos / d x_k
+  const R gjx = (k.ux - j.ux * cs) * j.ir, gjy = (k.uy - j.uy * cs) * j.ir,
+          gjz = (k.uz - j.uz * cs) * j.ir;
+  const R gkx = (j.ux - k.ux * cs) * k.ir, gky = (j.uy - k.uy * cs) * k.ir,
+          gkz = (j.uz - k.uz * cs) * k.ir;
+  o.jx = gjx * fgd + j.ux * fge;
+  o.jy = gjy * fgd + j.uy * fge;
+  o.jz = gjz * fgd + j.uz * fge;
+  const R ck = cge - fge;
+  o.kx = k.ux * ck + gkx * fgd;
+  o.ky = k.uy * ck + gky * fgd;
+  o.kz = k.uz * ck + gkz * fgd;
+  return o;
+}
+
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FUSED>
+__global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceArgs<R> a) {
+  constexpr bool kCache = G <= 8;     // register cache of d zeta / d x_k
+  constexpr int kUnroll = kCache ? G : 2;
+  constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
+  constexpr unsigned kGroupMask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
+  __shared__ double scut[SPEC == kSingle ? 1 : kRows];
+  __shared__ Stage<R> st;
+  __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
+  // fused filter: compacted short-list records, slot-indexed
+  __shared__ int s_j[FUSED ? kBlock : 1];
+  __shared__ double2 s_d01[FUSED ? kBlock : 1];   // dx, dy
+  __shared__ double2 s_d2r[FUSED ? kBlock : 1];   // dz, r^2
+  __shared__ double s_red[kBlock / 32][kRedWidth];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  Acc e_acc = 0;
+  Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
+
+  const int n_ovf = OVF ? a.flags[1] : 0;
+  if (OVF && n_ovf == 0) {              // nothing queued: leave a zero partial
+    if (tid < kRedWidth)
+      a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
+    return;
+  }
+
+  const int ns = a.ns;
+  const Row<R>* rows = static_cast<const Row<R>*>(a.rows);
+  const Row<R>& row0 = a.row0;
+  const double cut0 = a.cut0;
+  if (SPEC != kSingle) {
+    for (int q = tid; q < ns * ns * ns; q += blockDim.x) {
+      srow[q] = rows[q];
+      scut[q] = a.cutsq[q];
+    }
+    __syncthreads();
+  }
+
+  const int gl = tid & (G - 1);
+  const int gbase = tid - gl;          // block-local thread id of slot 0
+  const int wbase = lane - gl;         // warp lane of slot 0
+  constexpr int kAtomsPerBlock = kBlock / G;
+  const int ntiles = (a.n_owned + kAtomsPerBlock - 1) / kAtomsPerBlock;
+  const int nwarps_total = gridDim.x * (kBlock / 32);
+  int work = OVF ? blockIdx.x * (kBlock / 32) + tid / 32 : blockIdx.x;
+
+  while (true) {
+    int i;
+    bool active;
+    if (OVF) {
+      if (work >= n_ovf) break;        // warp-uniform
+      i = a.overflow[work];
+      active = true;
+    } else {
+      if (work >= ntiles) break;       // block-uniform
+      i = work * kAtomsPerBlock + tid / G;
+      active = i < a.n_owned;
+    }
+
+    const double4 pi = a.pos[active ? i : 0];
+    int n_i = 0;
+    if constexpr (FUSED) {
+      // The paper's cutoff filter (Sec. 4.4; neighbor.cpp:143-152) in-kernel:
+      // the group tests G skin entries per round with the reference's exact
+      // FP64 distance, and ballot + popc compacts the survivors into slots.
+      const int m = active ? a.skin_cnt[i] : 0;
+      const int mmax = __reduce_max_sync(kFull, m);
+      constexpr int kDepth = 4;          // rounds whose loads are in flight together
+      for (int c0 = 0; c0 < mmax; c0 += kDepth * G) {
+        int bb[kDepth];
+        double4 pb[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+          const int s = c0 + u * G + gl;
+          bb[u] = s < m ? a.skin[std::size_t(s) * a.npad + i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) pb[u] = a.pos[bb[u] >= 0 ? bb[u] : 0];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+          double ex_ = 0, ey_ = 0, ez_ = 0, er2 = 0;
+          bool pass = false;
+          if (bb[u] >= 0) {
+            displacement(pi, pb[u], a.box, ex_, ey_, ez_);
+            er2 = norm_sq_exact(ex_, ey_, ez_);
+            pass = er2 <= a.rc2;
+          }
+          const unsigned gm = (__ballot_sync(kFull, pass) >> wbase) & kGroupMask;
+          const int q = n_i + __popc(gm & ((1u << gl) - 1u));
+          if (pass) {
+            if (q < G) {
+              s_j[gbase + q] = bb[u];
+              s_d01[gbase + q] = make_double2(ex_, ey_);
+              s_d2r[gbase + q] = make_double2(ez_, er2);
+            }
+            a.short_out[std::size_t(q) * a.npad + i] = bb[u];
+          }
+          n_i += __popc(gm);
+        }
+      }
+      if (active && gl == 0) a.short_cnt_out[i] = n_i;
+      __syncwarp();
+    } else {
+      n_i = active ? a.cnt[i] : 0;
+    }
+    if (n_i > G) {
+      if (gl == 0) {
+        if (OVF) atomicOr(a.flags, kErrShortOverflow);
+        else a.overflow[atomicAdd(a.flags + 1, 1)] = i;
+      }
+      n_i = 0;
+      active = false;
+    }
+    const bool slot = gl < n_i;
+    int j;
+    double dx = 0, dy = 0, dz = 0, r2 = 1.0;
+    if constexpr (FUSED) {
+      j = slot ? s_j[tid] : (active ? i : 0);
+      if (slot) {
+        const double2 d01 = s_d01[tid], d2r = s_d2r[tid];
+        dx = d01.x;
+        dy = d01.y;
+        dz = d2r.x;
+        r2 = d2r.y;
+      }
+    } else {
+      j = slot ? a.nbr[std::size_t(gl) * a.npad + i] : (active ? i : 0);
+      if (slot) {
+        displacement(pi, a.pos[j], a.box, dx, dy, dz);
+        r2 = norm_sq_exact(dx, dy, dz);
+      }
+    }
+    const int si = SPEC == kSingle ? 0 : species_of(pi);
+    const int sj = SPEC == kSingle ? 0 : species_of(a.pos[j]);
+    const int row_jj = (si * ns + sj) * ns + sj;
+    const bool pair_ok = slot && r2 <= (SPEC == kSingle ? cut0 : scut[row_jj]);
+    const Row<R>& pjj = SPEC == kSingle ? row0 : srow[row_jj];
+
+    Nbr<R> me;
+    me.r = Fn<R>::sqrt_(R(r2));
+    me.ir = R(1) / me.r;
+    me.ux = R(dx) * me.ir;
+    me.uy = R(dy) * me.ir;
+    me.uz = R(dz) * me.ir;
+    R fc, dfc;
+    cutoff_ramp(me.r, pjj, fc, dfc);
+    // meta: species of this slot as a k, or -1 when it can never be one.
+    // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
+    // exactly "pair (i, k) inside its own cutoff".
+    const int meta = SPEC == kGeneric ? (slot ? sj : -1) : (pair_ok ? sj : -1);
+    st.put(tid, me, fc, dfc, meta);
+    if (SPEC == kGeneric) s_r2[tid] = r2;
+    __syncwarp();
+
+    const int rowbase = (si * ns + sj) * ns;
+
+    // ---- zeta pass: partner k = slot (l + t) mod n_i ----
+    R zeta = 0, gjx = 0, gjy = 0, gjz = 0;
+    R ckx[kCache ? G : 1], cky[kCache ? G : 1], ckz[kCache ? G : 1];
+#pragma unroll kUnroll
+    for (int t = 1; t < G; ++t) {
+      int m = gl + t;
+      if (m >= n_i) m -= n_i;
+      const int src = gbase + (m & (G - 1));
+      Nbr<R> k;
+      R fck, dfck, kmeta;
+      st.get(src, k, fck, dfck, kmeta);
+      bool ok = pair_ok && t < n_i && kmeta >= R(0);
+      const Row<R>* prow = &pjj;
+      if (SPEC != kSingle) {
+        const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+        prow = &srow[rowbase + sk];
+        if (SPEC == kGeneric) {
+          ok = ok && s_r2[src] <= scut[rowbase + sk];
+          cutoff_ramp(k.r, *prow, fck, dfck);
+        }
+      }
+      const Grad<R> tr = triplet<R>(me, k, fck, dfck, *prow);
+      zeta += ok ? tr.z : R(0);
+      gjx += ok ? tr.jx : R(0);
+      gjy += ok ? tr.jy : R(0);
+      gjz += ok ? tr.jz : R(0);
+      if constexpr (kCache) {
+        ckx[t] = ok ? tr.kx : R(0);
+        cky[t] = ok ? tr.ky : R(0);
+        ckz[t] = ok ? tr.kz : R(0);
+      }
+    }
+
+    // ---- pair block (potential.hpp:204-222) ----
+    R dvdr = 0, dvdz = 0, v = 0;
+    if (pair_ok) {
+      const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
+      const R dfr = -pjj.lam1 * fr;
+      const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
+      const R dfa = -pjj.lam2 * fa;
+      R b, db;
+      bond_order(zeta, pjj, b, db);
+      const R rep = fr + b * fa;
+      v = R(0.5) * fc * rep;
+      dvdr = R(0.5) * (dfc * rep + fc * (dfr + b * dfa));
+      dvdz = R(0.5) * fc * fa * db;
+      if (!isfinite(v) || !isfinite(dvdr) || !isfinite(dvdz)) atomicOr(a.flags, kErrNonFinite);
+    }
+    R px = -(me.ux * dvdr) - gjx * dvdz;
+    R py = -(me.uy * dvdr) - gjy * dvdz;
+    R pz = -(me.uz * dvdr) - gjz * dvdz;
+
+    // ---- scatter pass: lane (l + t) mod n receives lane l's k-gradient ----
+#pragma unroll kUnroll
+    for (int t = 1; t < G; ++t) {
+      R sx, sy, sz;
+      if constexpr (kCache) {
+        sx = ckx[t] * dvdz;
+        sy = cky[t] * dvdz;
+        sz = ckz[t] * dvdz;
+      } else {
+        int m = gl + t;
+        if (m >= n_i) m -= n_i;
+        const int src = gbase + (m & (G - 1));
+        Nbr<R> k;
+        R fck, dfck, kmeta;
+        st.get(src, k, fck, dfck, kmeta);
+        bool ok = pair_ok && t < n_i && kmeta >= R(0);
+        const Row<R>* prow = &pjj;
+        if (SPEC != kSingle) {
+          const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+          prow = &srow[rowbase + sk];
+          if (SPEC == kGeneric) {
+            ok = ok && s_r2[src] <= scut[rowbase + sk];
+            cutoff_ramp(k.r, *prow, fck, dfck);
+          }
+        }
+        const Grad<R> tr = triplet<R>(me, k, fck, dfck, *prow);
+        sx = ok ? tr.kx * dvdz : R(0);
+        sy = ok ? tr.ky * dvdz : R(0);
+        sz = ok ? tr.kz * dvdz : R(0);
+      }
+      int s = gl - t;
+      if (s < 0) s += n_i;
+      const int from = wbase + (s & (G - 1));
+      const R rx = __shfl_sync(kFull, sx, from);
+      const R ry = __shfl_sync(kFull, sy, from);
+      const R rz = __shfl_sync(kFull, sz, from);
+      const bool take = slot && t < n_i;
+      px -= take ? rx : R(0);
+      py -= take ? ry : R(0);
+      pz -= take ? rz : R(0);
+    }
+    if (!slot) px = py = pz = 0;
+
+    // F_i = -sum over the group's slots
+    R fx = px, fy = py, fz = pz;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      fx += __shfl_xor_sync(kFull, fx, o);
+      fy += __shfl_xor_sync(kFull, fy, o);
+      fz += __shfl_xor_sync(kFull, fz, o);
+    }
+
+    if (slot) {
+      e_acc += Acc(v);
+      const R rx = R(dx), ry = R(dy), rz = R(dz);
+      w_acc[0] += Acc(rx * px);
+      w_acc[1] += Acc(ry * py);
+      w_acc[2] += Acc(rz * pz);
+      w_acc[3] += Acc(rx * py);
+      w_acc[4] += Acc(rx * pz);
+      w_acc[5] += Acc(ry * pz);
+      if (DET) {
+        const std::size_t q = std::size_t(gl) * a.npad + i;
+        static_cast<Acc*>(a.slot_x)[q] = Acc(px);
+        static_cast<Acc*>(a.slot_y)[q] = Acc(py);
+        static_cast<Acc*>(a.slot_z)[q] = Acc(pz);
+      } else {
+        Acc* f = static_cast<Acc*>(a.forces) + 3 * std::size_t(j);
+        atomicAdd(f + 0, Acc(px));
+        atomicAdd(f + 1, Acc(py));
+        atomicAdd(f + 2, Acc(pz));
+      }
+    }
+    if (active && gl == 0) {
+      if (DET) {
+        Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+        f[0] = Acc(-fx);
+        f[1] = Acc(-fy);
+        f[2] = Acc(-fz);
+      } else {
+        Acc* f = static_cast<Acc*>(a.forces) + 3 * std::size_t(i);
+        atomicAdd(f + 0, Acc(-fx));
+        atomicAdd(f + 1, Acc(-fy));
+        atomicAdd(f + 2, Acc(-fz));
+      }
+    }
+    work += OVF ? nwarps_total : gridDim.x;
+    __syncwarp();                      // staging is rewritten by the next tile
+  }
+
+  // ---- block reduction of energy + virial, fixed order ----
+  double red[7] = {double(e_acc), double(w_acc[0]), double(w_acc[1]), double(w_acc[2]),
+                   double(w_acc[3]), double(w_acc[4]), double(w_acc[5])};
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) red[q] += __shfl_down_sync(kFull, red[q], o);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) s_red[tid / 32][q] = red[q];
+  __syncthreads();
+  if (tid < kRedWidth) {
+    double s = 0;
+    if (tid < 7)
+      for (int w = 0; w < kBlock / 32; ++w) s += s_red[w][tid];
+    a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = s;
+  }
+}
+
+// Sum of the block partials in a fixed order.
+__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partials, int nblocks,
+                                               double* __restrict__ out) {
+  __shared__ double s[256][7];
+  const int t = threadIdx.x;
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = t; b < nblocks; b += 256)
+    for (int q = 0; q < 7; ++q) acc[q] += partials[std::size_t(b) * kRedWidth + q];
+  for (int q = 0; q < 7; ++q) s[t][q] = acc[q];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (t < w)
+      for (int q = 0; q < 7; ++q) s[t][q] += s[t + w][q];
+    __syncthreads();
+  }
+  if (t < 7) out[t] = s[0][t];
+}
+
+// Deterministic scatter: F_a = F_self(a) + sum over a's short neighbours b of
+// the slot b wrote for a (lists are symmetric).
+template <typename Acc>
+__global__ void __launch_bounds__(kBlock) k_gather(int n, int npad, const int* __restrict__ nbr,
+                                                   const int* __restrict__ cnt,
+                                                   const Acc* __restrict__ sx,
+                                                   const Acc* __restrict__ sy,
+                                                   const Acc* __restrict__ sz,
+                                                   const Acc* __restrict__ fself,
+                                                   double* __restrict__ out) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  Acc fx = fself[3 * std::size_t(a)], fy = fself[3 * std::size_t(a) + 1],
+      fz = fself[3 * std::size_t(a) + 2];
+  const int m = cnt[a];
+  for (int s = 0; s < m; ++s) {
+    const int b = nbr[std::size_t(s) * npad + a];
+    const int mb = cnt[b];
+    for (int t = 0; t < mb; ++t) {
+      if (nbr[std::size_t(t) * npad + b] == a) {
+        const std::size_t q = std::size_t(t) * npad + b;
+        fx += sx[q];
+        fy += sy[q];
+        fz += sz[q];
+        break;
+      }
+    }
+  }
+  out[3 * std::size_t(a)] = double(fx);
+  out[3 * std::size_t(a) + 1] = double(fy);
+  out[3 * std::size_t(a) + 2] = double(fz);
+}
+
+__global__ void k_to_double(const float* __restrict__ in, double* __restrict__ out,
+                            std::size_t m) {
+  const std::size_t q = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < m) out[q] = double(in[q]);
+}
+
+template <typename R>
+Row<R> make_row(const Entry& e) {
+  Row<R> r{};
+  const double pi = 3.14159265358979323846;
+  r.a = R(e.big_a);
+  r.b = R(e.big_b);
+  r.lam1 = R(e.lambda1);
+  r.lam2 = R(e.lambda2);
+  r.lam3 = R(e.lambda3);
+  r.m3 = R(e.m == 3 ? 1 : 0);
+  r.beta = R(e.beta);
+  r.eta = R(e.eta);
+  r.nhie = R(-0.5 / e.eta);
+  r.big_r = R(e.big_r);
+  r.inv2d = R(0.5 / e.big_d);
+  r.rmd = R(e.big_r - e.big_d);
+  r.rpd = R(e.big_r + e.big_d);
+  r.nqd = R(-pi / 4 / e.big_d);
+  const double c2 = e.c * e.c, d2 = e.d * e.d;
+  r.gamma = R(e.gamma);
+  r.gcd2 = R(e.gamma * c2 / d2);
+  r.gc2 = R(e.gamma * c2);
+  r.d2 = R(d2);
+  r.h = R(e.h);
+  return r;
+}
+
+int ceil_div(std::int64_t a, int b) { return int((a + b - 1) / b); }
+
+// Persistent grid: resident blocks per SM x SM count, capped by the tile count.
+template <typename K>
+int persistent_blocks(K kernel, int tiles) {
+  static std::map<const void*, int> cache;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  int per_sm;
+  if (it == cache.end()) {
+    TSF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+    per_sm = std::max(1, per_sm);
+    cache[key] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  int dev = 0, sms = 148;
+  TSF_CUDA(cudaGetDevice(&dev));
+  TSF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return std::max(1, std::min(tiles, per_sm * sms));
+}
+
+constexpr int kOverflowBlocks = 148;
+
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool FUSED>
+int launch_main(Ctx& c, ForceArgs<R> a) {
+  const int tiles = std::max(1, ceil_div(a.n_owned, kBlock / G));
+  auto kern = k_force<R, Acc, G, SPEC, DET, false, FUSED>;
+  const int blocks = persistent_blocks(kern, tiles);
+  a.partial_base = 0;
+  c.mark(2);
+  kern<<<blocks, kBlock, 0, c.stream>>>(a);
+  c.mark(3);
+  ++c.launches;
+  return blocks;
+}
+
+template <typename R, typename Acc, int SPEC, bool DET, bool FUSED>
+void run_force(Ctx& c, ForceArgs<R> a) {
+  // Group width from the largest short count seen at the last list build;
+  // atoms that outgrow it between rebuilds take the overflow launch.
+  const int mx = std::max(1, c.short_list.max_count);
+  const int g = mx <= 4 ? 4 : mx <= 8 ? 8 : mx <= 16 ? 16 : 32;
+  int nb = 0;
+  switch (g) {
+    case 4: nb = launch_main<R, Acc, 4, SPEC, DET, FUSED>(c, a); break;
+    case 8: nb = launch_main<R, Acc, 8, SPEC, DET, FUSED>(c, a); break;
+    case 16: nb = launch_main<R, Acc, 16, SPEC, DET, FUSED>(c, a); break;
+    default: nb = launch_main<R, Acc, 32, SPEC, DET, FUSED>(c, a); break;
+  }
+  a.partial_base = nb;
+  k_force<R, Acc, 32, SPEC, DET, true, FUSED><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
+  k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb + kOverflowBlocks, c.result.get());
+  c.launches += 2;
+}
+
+template <typename R, typename Acc, bool DET, bool FUSED>
+void dispatch_spec(Ctx& c, const ForceArgs<R>& a) {
+  if (c.params.species_count() == 1) run_force<R, Acc, kSingle, DET, FUSED>(c, a);
+  else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET, FUSED>(c, a);
+  else run_force<R, Acc, kGeneric, DET, FUSED>(c, a);
+}
+
+template <typename R, typename Acc, bool DET>
+void dispatch_fused(Ctx& c, const ForceArgs<R>& a, bool fused) {
+  if (fused) dispatch_spec<R, Acc, DET, true>(c, a);
+  else dispatch_spec<R, Acc, DET, false>(c, a);
+}
+
+template <typename R, typename Acc>
+void compute_t(Ctx& c, std::uint32_t flags) {
+  const bool det = (flags & 0x1u) != 0;
+  const std::size_t n = std::size_t(c.n);
+  const int npad = c.npad;
+  const int cap = c.short_list.cap;
+
+  ForceArgs<R> a{};
+  a.row0 = make_row<R>(c.params.entry(0, 0, 0));
+  a.cut0 = c.params.entry(0, 0, 0).cutoff() * c.params.entry(0, 0, 0).cutoff();
+  a.pos = c.pos.get();
+  a.n_owned = int(c.n);
+  a.npad = npad;
+  a.box = c.box;
+  // fused: the kernel filters the skin list itself and writes the short list
+  const bool fused = (flags & 0x2u) == 0 && c.fuse_filter;
+  a.nbr = c.short_list.nbr.get();
+  a.cnt = c.short_list.cnt.get();
+  a.skin = c.skin_list.nbr.get();
+  a.skin_cnt = c.skin_list.cnt.get();
+  a.short_out = c.short_list.nbr.get();
+  a.short_cnt_out = c.short_list.cnt.get();
+  a.rc2 = c.params.r_cut_max() * c.params.r_cut_max();
+  a.rows = std::is_same<R, double>::value ? static_cast<const void*>(c.rows_f64.get())
+                                          : static_cast<const void*>(c.rows_f32.get());
+  a.cutsq = c.cutsq.get();
+  a.ns = c.params.species_count();
+  a.flags = c.flags.get();
+  c.overflow.reserve(std::max<std::size_t>(n, 1));
+  a.overflow = c.overflow.get();
+  c.partials.reserve(std::size_t(32 * 148 + kOverflowBlocks + 8) * kRedWidth);
+  a.partials = c.partials.get();
+  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 2 * sizeof(int), c.stream));
+
+  constexpr bool kF32 = std::is_same<Acc, float>::value;
+  if (det) {
+    const std::size_t words = std::size_t(cap) * npad * sizeof(Acc) / sizeof(double) + 1;
+    c.px.reserve(words);
+    c.py.reserve(words);
+    c.pz.reserve(words);
+    c.fself.reserve(3 * n * sizeof(Acc) / sizeof(double) + 1);
+    a.slot_x = c.px.get();
+    a.slot_y = c.py.get();
+    a.slot_z = c.pz.get();
+    a.fself = c.fself.get();
+    dispatch_fused<R, Acc, true>(c, a, fused);
+    if (n > 0) {
+      k_gather<Acc><<<ceil_div(n, kBlock), kBlock, 0, c.stream>>>(
+          int(n), npad, a.nbr, a.cnt, static_cast<const Acc*>(a.slot_x),
+          static_cast<const Acc*>(a.slot_y), static_cast<const Acc*>(a.slot_z),
+          static_cast<const Acc*>(a.fself), c.forces.get());
+      ++c.launches;
+    }
+  } else {
+    Acc* target;
+    if (kF32) {
+      c.fself.reserve(3 * n * sizeof(float) / sizeof(double) + 1);
+      target = reinterpret_cast<Acc*>(c.fself.get());
+    } else {
+      target = reinterpret_cast<Acc*>(c.forces.get());
+    }
+    TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
+    a.forces = target;
+    dispatch_fused<R, Acc, false>(c, a, fused);
+    if (kF32 && n > 0) {
+      k_to_double<<<ceil_div(3 * n, 256), 256, 0, c.stream>>>(
+          reinterpret_cast<const float*>(target), c.forces.get(), 3 * n);
+      ++c.launches;
+    }
+  }
+}
+
+}  // namespace
+
+}  // namespace tsf
