@@ -134,6 +134,7 @@ void upload_xyz(Ctx& c, const double* xyz) {
   }
   TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), src, m * sizeof(double), cudaMemcpyHostToDevice,
                            c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 5, 0, sizeof(int), c.stream));  // |coord| max
   tsf::pack_positions(c);
   c.forces_current = false;
 }
@@ -149,12 +150,17 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     geometry_changed |= c.box.len[ax] != box[ax] || c.box.per[ax] != int(per[ax] != 0);
     c.box.len[ax] = box[ax];
     c.box.per[ax] = per[ax] != 0;
+    c.boxf.len[ax] = float(box[ax]);
+    c.boxf.half[ax] = 0.5f * float(box[ax]);
+    c.boxf.per[ax] = c.box.per[ax];
   }
   if (n != c.n) {
     c.n = n;
+    c.sorted = false;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
     c.pos.reserve(nn);
+    c.posf.reserve(nn);
     c.species.reserve(nn);
     c.xyz_stage.reserve(3 * nn);
     c.forces.reserve(3 * nn);
@@ -164,6 +170,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
   if (geometry_changed) {
     c.skin_list.valid = false;
     c.short_list.valid = false;
+    c.tiled = false;
   }
   // species change rarely: re-upload only when they differ from the last upload
   if (n > 0 && (c.host_species.size() != std::size_t(n) ||
@@ -179,15 +186,16 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
 void download_forces(Ctx& c, double* forces) {
   const std::size_t m = 3 * std::size_t(c.n);
   if (m == 0) return;
+  tsf::unpack_forces(c);  // slot order -> user order
   if (is_pinned(forces)) {
-    TSF_CUDA(cudaMemcpyAsync(forces, c.forces.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c.stream));
+    TSF_CUDA(cudaMemcpyAsync(forces, c.forces_user.get(), m * sizeof(double),
+                             cudaMemcpyDeviceToHost, c.stream));
     TSF_CUDA(cudaStreamSynchronize(c.stream));
     return;
   }
   tsf::ensure_pinned(c, m);
-  TSF_CUDA(cudaMemcpyAsync(c.pinned, c.forces.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
-                           c.stream));
+  TSF_CUDA(cudaMemcpyAsync(c.pinned, c.forces_user.get(), m * sizeof(double),
+                           cudaMemcpyDeviceToHost, c.stream));
   TSF_CUDA(cudaStreamSynchronize(c.stream));
   std::memcpy(forces, c.pinned, m * sizeof(double));
 }
@@ -443,6 +451,9 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
   return guard(&ctx->c, [&] {
     Ctx& c = ctx->c;
     if (offsets[0] != 0) throw tsf::ConfigError("neighbor offsets must start at 0");
+    tsf::unsort(c);  // an external list speaks user indices: slot == user index
+    c.short_list.valid = false;
+    c.tiled = false;
     int mx = 0;
     for (std::int64_t a = 0; a < c.n; ++a) {
       const int len = offsets[a + 1] - offsets[a];
@@ -501,14 +512,25 @@ int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbr
     const tsf::ListState& s = list_for(c, which);
     std::vector<int> cnt;
     const std::vector<int> ell = download_ell(c, s, cnt);
+    // slot space -> user indices; segments ascending by user index
+    // (neighbor.cpp:114; the filter keeps that order, neighbor.cpp:143-152)
+    std::vector<int> perm(std::size_t(c.n)), slot_of(std::size_t(c.n));
+    if (c.sorted && c.n > 0) {
+      TSF_CUDA(cudaMemcpy(perm.data(), c.perm.get(), sizeof(int) * c.n, cudaMemcpyDeviceToHost));
+    } else {
+      for (std::int64_t q = 0; q < c.n; ++q) perm[std::size_t(q)] = int(q);
+    }
+    for (std::int64_t q = 0; q < c.n; ++q) slot_of[std::size_t(perm[std::size_t(q)])] = int(q);
     std::int64_t w = 0;
     offsets[0] = 0;
-    for (std::int64_t a = 0; a < c.n; ++a) {
-      for (int q = 0; q < cnt[std::size_t(a)]; ++q) {
-        if (w >= cap) throw tsf::ConfigError("neighbor export buffer too small");
-        nbrs[w++] = ell[std::size_t(q) * c.npad + a];
-      }
-      offsets[a + 1] = int32_t(w);
+    for (std::int64_t u = 0; u < c.n; ++u) {
+      const int a = slot_of[std::size_t(u)];
+      const int m = cnt[std::size_t(a)];
+      if (w + m > cap) throw tsf::ConfigError("neighbor export buffer too small");
+      for (int q = 0; q < m; ++q) nbrs[w + q] = perm[std::size_t(ell[std::size_t(q) * c.npad + a])];
+      std::sort(nbrs + w, nbrs + w + m);
+      w += m;
+      offsets[u + 1] = int32_t(w);
     }
   });
 }
@@ -552,8 +574,9 @@ int tsf_md_set_state(tsf_ctx* ctx, const double* vel, const double* masses) {
     if (m == 0) return;
     tsf::ensure_pinned(c, m);
     std::memcpy(c.pinned, vel, m * sizeof(double));
-    TSF_CUDA(cudaMemcpyAsync(c.vel.get(), c.pinned, m * sizeof(double), cudaMemcpyHostToDevice,
-                             c.stream));
+    TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), c.pinned, m * sizeof(double),
+                             cudaMemcpyHostToDevice, c.stream));
+    tsf::pack_velocities(c);
     TSF_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
@@ -566,8 +589,9 @@ int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel) {
     const std::size_t m = 3 * std::size_t(c.n);
     if (m == 0) return;
     tsf::ensure_pinned(c, m);
-    TSF_CUDA(cudaMemcpyAsync(c.pinned, c.vel.get(), m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c.stream));
+    tsf::unpack_velocities(c);
+    TSF_CUDA(cudaMemcpyAsync(c.pinned, c.xyz_stage.get(), m * sizeof(double),
+                             cudaMemcpyDeviceToHost, c.stream));
     TSF_CUDA(cudaStreamSynchronize(c.stream));
     std::memcpy(vel, c.pinned, m * sizeof(double));
   });

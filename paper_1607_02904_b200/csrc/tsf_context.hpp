@@ -49,7 +49,10 @@ struct Ctx {
   Params params;
   bool has_potential = true;   // false: list-only context (tsf_create with NULL params)
   bool hoist_ramp = true;
-  bool fuse_filter = true;     // filter inside the force kernel (env TSF_FUSE_FILTER=0: separate)
+  // Filter inside the force kernel (env TSF_FUSE_FILTER=1).  Off by default:
+  // measured slower at 2M atoms (0.90 vs 0.66 ms, f64) because the gather
+  // latency lands in the low-occupancy FP64 kernel (profiles/r01).
+  bool fuse_filter = false;
   std::string err;
   std::int64_t launches = 0;
 
@@ -62,12 +65,25 @@ struct Ctx {
   std::int64_t n = 0;
   int npad = 0;
   Box box{};
-  DevBuf<int> species;         // [n]
+  // Atoms live in HBM in cell-sorted order ("slots"), re-sorted at every list
+  // build with the key (cell, user index); perm maps slot -> user index.  The
+  // user order is restored only at the I/O boundary (pack / unpack / forces).
+  DevBuf<int> species;         // [n] user order
   std::vector<int> host_species;  // last uploaded species ids
-  DevBuf<double4> pos;         // {x, y, z, species}
+  DevBuf<int> perm;            // [n] slot -> user index
+  bool sorted = false;         // false: perm is the identity (slot == user index)
+  DevBuf<double4> pos;         // [n] slot order {x, y, z, species}
+  DevBuf<float4> posf;         // [n] slot order float shadow for the cutoff pre-tests
+  BoxF boxf{};
   DevBuf<double4> pos_ref;     // positions at the last list build (needs_rebuild)
-  DevBuf<double> xyz_stage;    // AoS staging for H2D / D2H
-  DevBuf<double> forces;       // [n][3]
+  DevBuf<double> xyz_stage;    // AoS staging for H2D / D2H, user order
+  DevBuf<double> forces;       // [n][3] slot order (accumulation, MD)
+  DevBuf<double> forces_user;  // [n][3] user order (download)
+  DevBuf<double4> tmp4;        // re-sort scratch
+  DevBuf<double> tmp3;
+  DevBuf<int> tmp_i;
+  DevBuf<unsigned long long> sort_keys, sort_keys_out;
+  DevBuf<int> sort_vals, sort_vals_out;
   double* pinned = nullptr;    // pinned host staging, pinned_cap doubles
   std::size_t pinned_cap = 0;
 
@@ -77,6 +93,8 @@ struct Ctx {
   bool short_max_stale = true; // re-read the largest short count after the next filter
   int short_apply = -1;        // filter mode of the current short list
   DevBuf<int> cell_of, cell_count, cell_start, cell_fill, binned;
+  CellGrid grid{};             // cell grid of the last build
+  bool tiled = false;          // slots are cell-sorted for `grid` (our own build)
   DevBuf<unsigned char> scan_tmp;
 
   // force scratch
@@ -123,8 +141,13 @@ void upload_params(Ctx& c);
 constexpr int kErrShortOverflow = 1;   // an atom has more than 32 short neighbours
 constexpr int kErrNonFinite = 2;       // non-finite pair term
 
-void pack_positions(Ctx& c);           // xyz_stage + species -> pos
-void unpack_positions(Ctx& c);         // pos -> xyz_stage
+void pack_positions(Ctx& c);           // xyz_stage + species (user order) -> pos (slots)
+void unpack_positions(Ctx& c);         // pos (slots) -> xyz_stage (user order)
+void unpack_forces(Ctx& c);            // forces (slots) -> forces_user
+void unsort(Ctx& c);                   // back to slot == user index (external lists)
+void refresh_shadow(Ctx& c);           // posf = float(pos)
+void pack_velocities(Ctx& c);          // xyz_stage (user order velocities) -> vel (slots)
+void unpack_velocities(Ctx& c);        // vel (slots) -> xyz_stage (user order)
 void md_kick(Ctx& c, double dt, bool drift);   // v += F dt/(2 m mvv2e) [; x += v dt, wrap]
 void md_kinetic(Ctx& c);               // KE -> result[7] (device)
 

@@ -20,6 +20,13 @@ struct Box {
   int per[3];
 };
 
+// Reference cell grid (neighbor.cpp:50-77): edge >= cutoff + skin.  Atoms are
+// stored sorted by cell id (cz ny + cy) nx + cx, so a cell is a slot range.
+struct CellGrid {
+  int nc[3];
+  double org[3], ext[3];
+};
+
 // minimum_image_1d(d, L) = d - L * floor(d / L + 0.5) (proj/include/tmd/box.hpp:28-30)
 // with the reference's exact rounding sequence: IEEE divide, no contraction.
 __device__ __forceinline__ double min_image_exact(double d, double len) {
@@ -51,6 +58,56 @@ __device__ __forceinline__ void displacement(const double4& a, const double4& b,
 }
 
 __device__ __forceinline__ int species_of(const double4& p) { return int(p.w); }
+
+// Float shadow of the positions (slot order, {x, y, z, species}) for cheap
+// pre-tests.  A pre-test decides "inside" / "outside" only when the float
+// squared distance clears the cutoff by more than its worst-case error
+// (`margin`, set from the coordinate magnitude, tsf::prefilter_margin); pairs
+// inside the band fall back to the exact FP64 test, so every decision is the
+// reference's.
+struct BoxF {
+  float len[3];
+  float half[3];
+  int per[3];
+};
+
+enum : int { kOut = 0, kIn = 1, kUnsure = 2 };
+
+// Largest |coordinate| ever packed into the shadow (float bits, atomicMax);
+// the pre-test bands are derived from it in-kernel, so no host round trip.
+__device__ __forceinline__ void track_coord_max(int* cmax, const double4& p) {
+  const float m = __double2float_ru(fmax(fabs(p.x), fmax(fabs(p.y), fabs(p.z))));
+  const unsigned act = __activemask();
+  const int v = __reduce_max_sync(act, __float_as_int(m));
+  if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(cmax, v);
+}
+
+// [lo, hi] around cut^2: outside it the float r^2 decides the cutoff test
+// exactly as FP64 would.  Error model: each float coordinate is off by <=
+// |x| 2^-24, the float displacement (with a float box wrap) by ed <=
+// (3 M + cut) 2^-24, the float r^2 by <= 2 sqrt(3) cut ed + 3 ed^2 + a few
+// float roundings of cut^2; doubled for safety.
+__device__ __forceinline__ void band_for(double cut, const int* cmax, float& lo, float& hi) {
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  const double M = double(__int_as_float(*cmax));
+  const double ed = (3.0 * M + cut) * u * 1.01;
+  const double er2 = 2.0 * (3.4641016151377544 * cut * ed + 3.0 * ed * ed + 8.0 * u * cut * cut);
+  lo = __double2float_rd(cut * cut - er2);
+  hi = __double2float_ru(cut * cut + er2);
+}
+
+__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const BoxF& box,
+                                         float lo, float hi) {
+  float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax)
+    if (box.per[ax]) {
+      if (d[ax] > box.half[ax]) d[ax] -= box.len[ax];
+      else if (d[ax] < -box.half[ax]) d[ax] += box.len[ax];
+    }
+  const float r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+  return r2 < lo ? kIn : (r2 > hi ? kOut : kUnsure);
+}
 
 
 }  // namespace tsf

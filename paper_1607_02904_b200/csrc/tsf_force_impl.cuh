@@ -54,7 +54,10 @@ struct ForceArgs {
   const int* skin_cnt;
   int* short_out;      // fused filter: short list written as a by-product
   int* short_cnt_out;
-  double rc2;          // r_cut_max^2 of the filter (neighbor.cpp:143-152)
+  double rc, rc2;      // r_cut_max (^2) of the filter (neighbor.cpp:143-152)
+  const float4* posf;  // float shadow for the pre-test
+  const int* cmax;     // |coordinate| bound for the pre-test band
+  BoxF boxf;
   const void* rows;
   const double* cutsq;
   int ns;
@@ -227,23 +230,27 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
       // FP64 distance, and ballot + popc compacts the survivors into slots.
       const int m = active ? a.skin_cnt[i] : 0;
       const int mmax = __reduce_max_sync(kFull, m);
+      float lo, hi;
+      band_for(a.rc, a.cmax, lo, hi);
+      const float4 pfi = a.posf[active ? i : 0];
       constexpr int kDepth = 4;          // rounds whose loads are in flight together
       for (int c0 = 0; c0 < mmax; c0 += kDepth * G) {
         int bb[kDepth];
-        double4 pb[kDepth];
+        float4 pb[kDepth];
 #pragma unroll
         for (int u = 0; u < kDepth; ++u) {
           const int s = c0 + u * G + gl;
           bb[u] = s < m ? a.skin[std::size_t(s) * a.npad + i] : -1;
         }
 #pragma unroll
-        for (int u = 0; u < kDepth; ++u) pb[u] = a.pos[bb[u] >= 0 ? bb[u] : 0];
+        for (int u = 0; u < kDepth; ++u) pb[u] = a.posf[bb[u] >= 0 ? bb[u] : 0];
 #pragma unroll
         for (int u = 0; u < kDepth; ++u) {
           double ex_ = 0, ey_ = 0, ez_ = 0, er2 = 0;
           bool pass = false;
-          if (bb[u] >= 0) {
-            displacement(pi, pb[u], a.box, ex_, ey_, ez_);
+          if (bb[u] >= 0 && prefilter(pfi, pb[u], a.boxf, lo, hi) != kOut) {
+            // survivors (and the rare band cases) get the exact FP64 distance
+            displacement(pi, a.pos[bb[u]], a.box, ex_, ey_, ez_);
             er2 = norm_sq_exact(ex_, ey_, ez_);
             pass = er2 <= a.rc2;
           }
@@ -652,7 +659,11 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.skin_cnt = c.skin_list.cnt.get();
   a.short_out = c.short_list.nbr.get();
   a.short_cnt_out = c.short_list.cnt.get();
+  a.rc = c.params.r_cut_max();
   a.rc2 = c.params.r_cut_max() * c.params.r_cut_max();
+  a.posf = c.posf.get();
+  a.cmax = c.flags.get() + 5;
+  a.boxf = c.boxf;
   a.rows = std::is_same<R, double>::value ? static_cast<const void*>(c.rows_f64.get())
                                           : static_cast<const void*>(c.rows_f32.get());
   a.cutsq = c.cutsq.get();

@@ -1,5 +1,6 @@
-// Position packing and the GPU-resident velocity-Verlet pieces
-// (proj/src/engine.cpp:142-166: half-kick, drift + wrap, ..., half-kick).
+// Slot <-> user-order movement at the I/O boundary and the GPU-resident
+// velocity-Verlet pieces (proj/src/engine.cpp:142-166: half-kick, drift + wrap,
+// ..., half-kick).
 #include "tsf_context.hpp"
 #include "tsf_units.hpp"
 
@@ -9,20 +10,65 @@ namespace {
 
 int blocks_for(std::int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
 
-__global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ species, int n,
-                       double4* __restrict__ pos) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  pos[a] = make_double4(xyz[3 * a], xyz[3 * a + 1], xyz[3 * a + 2], double(species[a]));
+// slot s holds user atom perm[s] (perm == nullptr: identity)
+__device__ __forceinline__ int user_of(const int* __restrict__ perm, int s) {
+  return perm ? perm[s] : s;
 }
 
-__global__ void k_unpack(const double4* __restrict__ pos, int n, double* __restrict__ xyz) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  const double4 p = pos[a];
-  xyz[3 * a] = p.x;
-  xyz[3 * a + 1] = p.y;
-  xyz[3 * a + 2] = p.z;
+__device__ __forceinline__ float4 shadow(const double4& p) {
+  return make_float4(float(p.x), float(p.y), float(p.z), float(p.w));
+}
+
+__global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ species,
+                       const int* __restrict__ perm, int n, double4* __restrict__ pos,
+                       float4* __restrict__ posf, int* __restrict__ cmax) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int u = user_of(perm, s);
+  const double4 p = make_double4(xyz[3 * u], xyz[3 * u + 1], xyz[3 * u + 2], double(species[u]));
+  pos[s] = p;
+  posf[s] = shadow(p);
+  track_coord_max(cmax, p);
+}
+
+__global__ void k_refresh_shadow(const double4* __restrict__ pos, int n,
+                                 float4* __restrict__ posf, int* __restrict__ cmax) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double4 p = pos[s];
+  posf[s] = shadow(p);
+  track_coord_max(cmax, p);
+}
+
+__global__ void k_unpack(const double4* __restrict__ pos, const int* __restrict__ perm, int n,
+                         double* __restrict__ xyz) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int u = user_of(perm, s);
+  const double4 p = pos[s];
+  xyz[3 * u] = p.x;
+  xyz[3 * u + 1] = p.y;
+  xyz[3 * u + 2] = p.z;
+}
+
+// out[perm[s]] = in[s] for 3-vectors (to user order), or out[s] = in[perm[s]]
+template <bool kToUser>
+__global__ void k_permute3(const double* __restrict__ in, const int* __restrict__ perm, int n,
+                           double* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int u = user_of(perm, s);
+  const int src = kToUser ? s : u, dst = kToUser ? u : s;
+  out[3 * dst] = in[3 * src];
+  out[3 * dst + 1] = in[3 * src + 1];
+  out[3 * dst + 2] = in[3 * src + 2];
+}
+
+__global__ void k_unsort_pos(const double4* __restrict__ in, const int* __restrict__ perm, int n,
+                             double4* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  out[perm[s]] = in[s];
 }
 
 // wrap_1d (box.hpp:41-46)
@@ -37,16 +83,16 @@ struct Masses {
   double m[kMaxSpecies];
 };
 
-__global__ void k_kick(double4* __restrict__ pos, double* __restrict__ vel,
-                       const double* __restrict__ f, int n, Masses ms, double dt, int drift,
-                       Box box) {
+__global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
+                       int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n, Masses ms,
+                       double dt, int drift, Box box) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   double4 p = pos[a];
   const double k = __ddiv_rn(__dmul_rn(0.5, dt), __dmul_rn(ms.m[species_of(p)], kMvv2e));
-  double vx = __dadd_rn(vel[3 * a], __dmul_rn(f[3 * a], k));
-  double vy = __dadd_rn(vel[3 * a + 1], __dmul_rn(f[3 * a + 1], k));
-  double vz = __dadd_rn(vel[3 * a + 2], __dmul_rn(f[3 * a + 2], k));
+  const double vx = __dadd_rn(vel[3 * a], __dmul_rn(f[3 * a], k));
+  const double vy = __dadd_rn(vel[3 * a + 1], __dmul_rn(f[3 * a + 1], k));
+  const double vz = __dadd_rn(vel[3 * a + 2], __dmul_rn(f[3 * a + 2], k));
   vel[3 * a] = vx;
   vel[3 * a + 1] = vy;
   vel[3 * a + 2] = vz;
@@ -58,6 +104,8 @@ __global__ void k_kick(double4* __restrict__ pos, double* __restrict__ vel,
     if (box.per[1]) p.y = wrap(p.y, box.len[1]);
     if (box.per[2]) p.z = wrap(p.z, box.len[2]);
     pos[a] = p;
+    posf[a] = shadow(p);
+    track_coord_max(cmax, p);
   }
 }
 
@@ -102,26 +150,83 @@ Masses masses_of(const Ctx& c) {
   return m;
 }
 
+const int* perm_of(const Ctx& c) { return c.sorted ? c.perm.get() : nullptr; }
+
 }  // namespace
 
 void pack_positions(Ctx& c) {
   if (c.n == 0) return;
   k_pack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.xyz_stage.get(), c.species.get(),
-                                                   int(c.n), c.pos.get());
+                                                   perm_of(c), int(c.n), c.pos.get(),
+                                                   c.posf.get(), c.flags.get() + 5);
+  ++c.launches;
+}
+
+void refresh_shadow(Ctx& c) {
+  if (c.n == 0) return;
+  k_refresh_shadow<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), int(c.n),
+                                                             c.posf.get(), c.flags.get() + 5);
   ++c.launches;
 }
 
 void unpack_positions(Ctx& c) {
   if (c.n == 0) return;
-  k_unpack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), int(c.n), c.xyz_stage.get());
+  k_unpack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), perm_of(c), int(c.n),
+                                                     c.xyz_stage.get());
   ++c.launches;
+}
+
+void unpack_forces(Ctx& c) {
+  if (c.n == 0) return;
+  c.forces_user.reserve(3 * std::size_t(c.n));
+  k_permute3<true><<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.forces.get(), perm_of(c),
+                                                             int(c.n), c.forces_user.get());
+  ++c.launches;
+}
+
+void pack_velocities(Ctx& c) {
+  if (c.n == 0) return;
+  k_permute3<false><<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.xyz_stage.get(), perm_of(c),
+                                                              int(c.n), c.vel.get());
+  ++c.launches;
+}
+
+void unpack_velocities(Ctx& c) {
+  if (c.n == 0) return;
+  k_permute3<true><<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.vel.get(), perm_of(c), int(c.n),
+                                                             c.xyz_stage.get());
+  ++c.launches;
+}
+
+void unsort(Ctx& c) {
+  if (!c.sorted || c.n == 0) {
+    c.sorted = false;
+    return;
+  }
+  const std::size_t n = std::size_t(c.n);
+  c.tmp4.reserve(n);
+  c.tmp3.reserve(3 * n);
+  const int* perm = c.perm.get();
+  k_unsort_pos<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), perm, int(c.n),
+                                                         c.tmp4.get());
+  TSF_CUDA(cudaMemcpyAsync(c.pos.get(), c.tmp4.get(), n * sizeof(double4),
+                           cudaMemcpyDeviceToDevice, c.stream));
+  k_permute3<true><<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.vel.get(), perm, int(c.n),
+                                                             c.tmp3.get());
+  TSF_CUDA(cudaMemcpyAsync(c.vel.get(), c.tmp3.get(), 3 * n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c.stream));
+  c.launches += 2;
+  c.sorted = false;
+  c.forces_current = false;
+  refresh_shadow(c);
 }
 
 void md_kick(Ctx& c, double dt, bool drift) {
   if (c.n == 0) return;
-  k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), c.vel.get(), c.forces.get(),
-                                                   int(c.n), masses_of(c), dt, drift ? 1 : 0,
-                                                   c.box);
+  k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), c.posf.get(),
+                                                   c.flags.get() + 5, c.vel.get(),
+                                                   c.forces.get(), int(c.n), masses_of(c), dt,
+                                                   drift ? 1 : 0, c.box);
   ++c.launches;
 }
 

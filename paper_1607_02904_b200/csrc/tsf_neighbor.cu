@@ -1,36 +1,40 @@
-// GPU cell-list neighbor build, the paper's cutoff filter (short list) and the
-// rebuild trigger.
+// GPU cell-list neighbor build with a cell-sorted atom layout, the paper's
+// cutoff filter (short list) and the rebuild trigger.
 //
 // Output contract (bit-exact with the reference):
 //   build_neighbor_list  proj/src/neighbor.cpp:37-132  — full, symmetric list of
-//     every b != a with |min_image(x_b - x_a)|^2 <= (rc + skin)^2, computed with
-//     the reference's FP64 rounding sequence (no contraction), segments sorted
-//     ascending by atom index.  The cell grid is the reference's (same edge,
-//     same binning arithmetic, same deduplicated 27-stencil), so even ulp-level
-//     binning decisions at cell faces select the same candidate set.
+//     every b != a with |min_image(x_b - x_a)|^2 <= (rc + skin)^2, decided with
+//     the reference's FP64 rounding sequence (no contraction).  The cell grid
+//     is the reference's (same edge, same binning arithmetic, same
+//     deduplicated 27-stencil), so even ulp-level binning decisions at cell
+//     faces select the same candidate set.  Exported segments are mapped back
+//     to user indices and sorted ascending (neighbor.cpp:114).
 //   filter_all_segments  proj/src/neighbor.cpp:143-180 — skin entries with
 //     r^2 <= r_cut_max^2, order kept; verbatim copy when the filter is off.
 //   needs_rebuild        proj/src/neighbor.cpp:134-141 — any |dx|^2 > (skin/2)^2.
 //
-// Storage: ELL, column-major (nbr[s * npad + a]) + count[a].  One thread per
-// atom; at every slot s a warp touches 32 consecutive words.
+// Layout and kernels:
+//   * every build re-sorts the atoms by (cell, user index) with a radix sort:
+//     a cell's atoms are a contiguous slot range, and threads of a warp
+//     (neighbouring atoms) gather the same cache lines;
+//   * candidates are tested on a float shadow of the positions (16 B gathers
+//     instead of 32 B) with a rigorous error band; only pairs inside the band
+//     take the exact FP64 test (tsf_device.cuh), so decisions stay bit-exact;
+//   * lists are ELL, column-major (nbr[s * npad + a]) + count[a], in slots.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "tsf_context.hpp"
 
 namespace tsf {
 
 namespace {
-
-struct Grid {
-  int nc[3];
-  double org[3], ext[3];
-};
 
 __device__ __forceinline__ int clamp_cell(double p, double org, double ext, int n) {
   // int(floor(((p - o) / e) * n)) clamped to [0, n-1]  (neighbor.cpp:19-28)
@@ -39,34 +43,47 @@ __device__ __forceinline__ int clamp_cell(double p, double org, double ext, int 
   return c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
 }
 
-__global__ void k_cell_count(const double4* __restrict__ pos, int n, Grid g,
-                             int* __restrict__ cell_of, int* __restrict__ count) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  const double4 p = pos[a];
-  const int cx = clamp_cell(p.x, g.org[0], g.ext[0], g.nc[0]);
-  const int cy = clamp_cell(p.y, g.org[1], g.ext[1], g.nc[1]);
-  const int cz = clamp_cell(p.z, g.org[2], g.ext[2], g.nc[2]);
-  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx;
-  cell_of[a] = c;
-  atomicAdd(count + c, 1);
-}
-
-__global__ void k_cell_fill(int n, const int* __restrict__ cell_of,
-                            const int* __restrict__ start, int* __restrict__ fill,
-                            int* __restrict__ binned) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  const int c = cell_of[a];
-  binned[start[c] + atomicAdd(fill + c, 1)] = a;
-}
-
-// atomicMax from one lane per converged subset: a per-thread atomic on one
-// address serializes at L2 (measured: 1.8 ms for 2M atoms).
+// atomicMax from one lane per converged subset.
 __device__ __forceinline__ void warp_atomic_max(int* p, int v) {
   const unsigned act = __activemask();
   const int m = __reduce_max_sync(act, v);
   if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(p, m);
+}
+
+// Sort key (cell, user index) per slot; counts per cell; largest occupancy.
+__global__ void k_cell_key(const double4* __restrict__ pos, const int* __restrict__ perm, int n,
+                           CellGrid g, unsigned long long* __restrict__ keys,
+                           int* __restrict__ vals, int* __restrict__ count,
+                           int* __restrict__ max_occ) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double4 p = pos[s];
+  const int cx = clamp_cell(p.x, g.org[0], g.ext[0], g.nc[0]);
+  const int cy = clamp_cell(p.y, g.org[1], g.ext[1], g.nc[1]);
+  const int cz = clamp_cell(p.z, g.org[2], g.ext[2], g.nc[2]);
+  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx;
+  const unsigned user = unsigned(perm ? perm[s] : s);
+  keys[s] = (static_cast<unsigned long long>(c) << 32) | user;
+  vals[s] = s;
+  warp_atomic_max(max_occ, atomicAdd(count + c, 1) + 1);
+}
+
+// Apply the new order: slot t takes old slot src[t].
+__global__ void k_reorder(const unsigned long long* __restrict__ keys,
+                          const int* __restrict__ src, int n, const double4* __restrict__ pos_in,
+                          const double* __restrict__ vel_in, double4* __restrict__ pos_out,
+                          double* __restrict__ vel_out, int* __restrict__ perm,
+                          int* __restrict__ cell_of) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int s = src[t];
+  const unsigned long long k = keys[t];
+  pos_out[t] = pos_in[s];
+  vel_out[3 * t] = vel_in[3 * s];
+  vel_out[3 * t + 1] = vel_in[3 * s + 1];
+  vel_out[3 * t + 2] = vel_in[3 * s + 2];
+  perm[t] = int(k & 0xffffffffull);
+  cell_of[t] = int(k >> 32);
 }
 
 // Unique wrapped neighbor coordinates along one axis (the per-axis factor of
@@ -84,42 +101,61 @@ __device__ __forceinline__ int axis_stencil(int c, int n, int per, int out[3]) {
   return m;
 }
 
+struct ListArgs {
+  const double4* pos;
+  const float4* posf;
+  const int* cmax;
+  int n, npad;
+  Box box;
+  BoxF boxf;
+  CellGrid g;
+  const int* cell_of;
+  const int* start;
+};
+
+// Skin list, one thread per slot: candidates are the stencil cells' slot
+// ranges (contiguous in the cell-sorted layout), tested on the float shadow
+// with the exact FP64 fallback inside the error band.
 template <int CAP>
-__global__ void __launch_bounds__(kBlock) k_skin_list(
-    const double4* __restrict__ pos, int n, int npad, Box box, Grid g, double bc2,
-    const int* __restrict__ cell_of, const int* __restrict__ start,
-    const int* __restrict__ binned, int cap, int* __restrict__ nbr, int* __restrict__ cnt,
-    int* __restrict__ max_count) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  const double4 pa = pos[a];
-  const int home = cell_of[a];
-  const int cx = home % g.nc[0], cy = (home / g.nc[0]) % g.nc[1], cz = home / (g.nc[0] * g.nc[1]);
+__global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, double bc2, int cap,
+                                                      int* __restrict__ nbr,
+                                                      int* __restrict__ cnt,
+                                                      int* __restrict__ max_count) {
+  const int at = blockIdx.x * blockDim.x + threadIdx.x;
+  if (at >= a.n) return;
+  float lo, hi;
+  band_for(bc, a.cmax, lo, hi);
+  const CellGrid& g = a.g;
+  const float4 pfa = a.posf[at];
+  const int home = a.cell_of[at];
+  const int cx = home % g.nc[0], cy = (home / g.nc[0]) % g.nc[1];
+  const int cz = home / (g.nc[0] * g.nc[1]);
   int sx[3], sy[3], sz[3];
-  const int mx = axis_stencil(cx, g.nc[0], box.per[0], sx);
-  const int my = axis_stencil(cy, g.nc[1], box.per[1], sy);
-  const int mz = axis_stencil(cz, g.nc[2], box.per[2], sz);
+  const int mx = axis_stencil(cx, g.nc[0], a.box.per[0], sx);
+  const int my = axis_stencil(cy, g.nc[1], a.box.per[1], sy);
+  const int mz = axis_stencil(cz, g.nc[2], a.box.per[2], sz);
   int buf[CAP];
   int m = 0;
-  for (int iz = 0; iz < mz; ++iz)
-    for (int iy = 0; iy < my; ++iy)
-      for (int ix = 0; ix < mx; ++ix) {
-        const int c = (sz[iz] * g.nc[1] + sy[iy]) * g.nc[0] + sx[ix];
-        for (int t = start[c]; t < start[c + 1]; ++t) {
-          const int b = binned[t];
-          if (b == a) continue;
-          double dx, dy, dz;
-          displacement(pa, pos[b], box, dx, dy, dz);
-          if (norm_sq_exact(dx, dy, dz) <= bc2) {
-            if (m < CAP) buf[m] = b;
-            ++m;
-          }
-        }
+  for (int q = 0; q < mx * my * mz; ++q) {
+    const int c = (sz[q / (mx * my)] * g.nc[1] + sy[(q / mx) % my]) * g.nc[0] + sx[q % mx];
+    const int b1 = a.start[c + 1];
+    for (int b = a.start[c]; b < b1; ++b) {
+      if (b == at) continue;
+      int v = prefilter(pfa, a.posf[b], a.boxf, lo, hi);
+      if (v == kUnsure) {
+        double dx, dy, dz;
+        displacement(a.pos[at], a.pos[b], a.box, dx, dy, dz);
+        v = norm_sq_exact(dx, dy, dz) <= bc2 ? kIn : kOut;
       }
+      if (v == kIn) {
+        if (m < CAP) buf[m] = b;
+        ++m;
+      }
+    }
+  }
   warp_atomic_max(max_count, m);
   if (m > cap || m > CAP) return;  // host grows the capacity and rebuilds
-  // ascending atom index (neighbor.cpp:114)
-  for (int i = 1; i < m; ++i) {
+  for (int i = 1; i < m; ++i) {    // ascending slot
     const int v = buf[i];
     int j = i - 1;
     while (j >= 0 && buf[j] > v) {
@@ -128,43 +164,52 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(
     }
     buf[j + 1] = v;
   }
-  for (int s = 0; s < m; ++s) nbr[std::size_t(s) * npad + a] = buf[s];
-  cnt[a] = m;
+  for (int s = 0; s < m; ++s) nbr[std::size_t(s) * a.npad + at] = buf[s];
+  cnt[at] = m;
 }
 
-// Short list: skin entries with r^2 <= r_cut_max^2 in segment order.
+// Short list, one thread per slot: skin entries with r^2 <= r_cut_max^2 in
+// segment order (float pre-test, exact FP64 inside the band), or a verbatim
+// copy when the filter is off.
 __global__ void __launch_bounds__(kBlock) k_filter(
-    const double4* __restrict__ pos, int n, int npad, Box box, double rc2, int apply,
-    const int* __restrict__ skin, const int* __restrict__ skin_cnt, int* __restrict__ out,
-    int* __restrict__ out_cnt, int* __restrict__ max_count) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  const int m = skin_cnt[a];
+    ListArgs a, double rc, double rc2, int apply, const int* __restrict__ skin,
+    const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
+    int* __restrict__ max_count) {
+  const int at = blockIdx.x * blockDim.x + threadIdx.x;
+  if (at >= a.n) return;
+  const int m = skin_cnt[at];
   int w = 0;
   if (apply) {
-    const double4 pa = pos[a];
+    float lo, hi;
+    band_for(rc, a.cmax, lo, hi);
+    const float4 pfa = a.posf[at];
     constexpr int kDepth = 4;   // loads in flight per thread
     for (int s0 = 0; s0 < m; s0 += kDepth) {
       int bb[kDepth];
-      double4 pb[kDepth];
+      float4 pb[kDepth];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u)
-        bb[u] = s0 + u < m ? skin[std::size_t(s0 + u) * npad + a] : -1;
+        bb[u] = s0 + u < m ? skin[std::size_t(s0 + u) * a.npad + at] : -1;
 #pragma unroll
-      for (int u = 0; u < kDepth; ++u) pb[u] = pos[bb[u] >= 0 ? bb[u] : a];
+      for (int u = 0; u < kDepth; ++u) pb[u] = a.posf[bb[u] >= 0 ? bb[u] : at];
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) {
         if (bb[u] < 0) continue;
-        double dx, dy, dz;
-        displacement(pa, pb[u], box, dx, dy, dz);
-        if (norm_sq_exact(dx, dy, dz) <= rc2) out[std::size_t(w++) * npad + a] = bb[u];
+        int v = prefilter(pfa, pb[u], a.boxf, lo, hi);
+        if (v == kUnsure) {
+          double dx, dy, dz;
+          displacement(a.pos[at], a.pos[bb[u]], a.box, dx, dy, dz);
+          v = norm_sq_exact(dx, dy, dz) <= rc2 ? kIn : kOut;
+        }
+        if (v == kIn) out[std::size_t(w++) * a.npad + at] = bb[u];
       }
     }
   } else {
-    for (int s = 0; s < m; ++s) out[std::size_t(s) * npad + a] = skin[std::size_t(s) * npad + a];
+    for (int s = 0; s < m; ++s)
+      out[std::size_t(s) * a.npad + at] = skin[std::size_t(s) * a.npad + at];
     w = m;
   }
-  out_cnt[a] = w;
+  out_cnt[at] = w;
   warp_atomic_max(max_count, w);
 }
 
@@ -209,12 +254,39 @@ double from_key(unsigned long long k) {
 
 int blocks_for(std::int64_t n) { return int((n + kBlock - 1) / kBlock); }
 
+template <typename T>
+void swap_buf(DevBuf<T>& a, DevBuf<T>& b) {
+  std::swap(a.ptr, b.ptr);
+  std::swap(a.cap, b.cap);
+}
+
+ListArgs list_args(Ctx& c) {
+  ListArgs a;
+  a.pos = c.pos.get();
+  a.posf = c.posf.get();
+  a.cmax = c.flags.get() + 5;
+  a.n = int(c.n);
+  a.npad = c.npad;
+  a.box = c.box;
+  a.boxf = c.boxf;
+  a.g = c.grid;
+  a.cell_of = c.cell_of.get();
+  a.start = c.cell_start.get();
+  return a;
+}
+
 template <int CAP>
-void launch_skin(Ctx& c, const Grid& g, double bc2, int cap) {
+void launch_skin(Ctx& c, double bc2, int cap) {
   k_skin_list<CAP><<<blocks_for(c.n), kBlock, 0, c.stream>>>(
-      c.pos.get(), int(c.n), c.npad, c.box, g, bc2, c.cell_of.get(), c.cell_start.get(),
-      c.binned.get(), cap, c.skin_list.nbr.get(), c.skin_list.cnt.get(), c.flags.get() + 3);
+      list_args(c), std::sqrt(bc2), bc2, cap, c.skin_list.nbr.get(), c.skin_list.cnt.get(),
+      c.flags.get() + 3);
   ++c.launches;
+}
+
+int bits_for(std::int64_t v) {
+  int b = 1;
+  while ((std::int64_t(1) << b) <= v) ++b;
+  return b;
 }
 
 }  // namespace
@@ -260,7 +332,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
       hi[ax] = std::max(mx, mn + bc);
     }
   }
-  Grid g;
+  CellGrid& g = c.grid;
   for (int ax = 0; ax < 3; ++ax) {
     g.org[ax] = lo[ax];
     g.ext[ax] = hi[ax] - lo[ax];
@@ -269,31 +341,55 @@ void list_build(Ctx& c, double cutoff, double skin) {
   const std::int64_t ncells = std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2];
   if (ncells > (1ll << 30)) throw ConfigError("cell grid too large");
 
-  c.cell_of.reserve(std::size_t(std::max(n, 1)));
-  c.binned.reserve(std::size_t(std::max(n, 1)));
+  // ---- re-sort the atoms by (cell, user index) ----
+  const std::size_t nn = std::size_t(std::max(n, 1));
+  c.cell_of.reserve(nn);
   c.cell_count.reserve(std::size_t(ncells) + 1);
   c.cell_start.reserve(std::size_t(ncells) + 1);
-  c.cell_fill.reserve(std::size_t(ncells) + 1);
-  TSF_CUDA(cudaMemsetAsync(c.cell_count.get(), 0, sizeof(int) * (ncells + 1), c.stream));
-  TSF_CUDA(cudaMemsetAsync(c.cell_fill.get(), 0, sizeof(int) * (ncells + 1), c.stream));
-  if (n > 0) {
-    k_cell_count<<<blocks_for(n), kBlock, 0, c.stream>>>(c.pos.get(), n, g, c.cell_of.get(),
-                                                         c.cell_count.get());
-    ++c.launches;
-  }
-  std::size_t tmp = 0;
-  TSF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.cell_count.get(), c.cell_start.get(),
+  c.sort_keys.reserve(nn);
+  c.sort_keys_out.reserve(nn);
+  c.sort_vals.reserve(nn);
+  c.sort_vals_out.reserve(nn);
+  c.perm.reserve(nn);
+  c.tmp4.reserve(nn);
+  c.tmp3.reserve(3 * nn);
+  const int end_bit = 32 + bits_for(ncells);
+  std::size_t t_sort = 0, t_scan = 0;
+  TSF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, c.sort_keys.get(),
+                                           c.sort_keys_out.get(), c.sort_vals.get(),
+                                           c.sort_vals_out.get(), std::max(n, 1), 0, end_bit,
+                                           c.stream));
+  TSF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, c.cell_count.get(), c.cell_start.get(),
                                          int(ncells + 1), c.stream));
-  c.scan_tmp.reserve(tmp);
-  TSF_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.get(), tmp, c.cell_count.get(),
+  c.scan_tmp.reserve(std::max(t_sort, t_scan));
+  TSF_CUDA(cudaMemsetAsync(c.cell_count.get(), 0, sizeof(int) * (ncells + 1), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 6, 0, sizeof(int), c.stream));
+  if (n > 0) {
+    k_cell_key<<<blocks_for(n), kBlock, 0, c.stream>>>(
+        c.pos.get(), c.sorted ? c.perm.get() : nullptr, n, g, c.sort_keys.get(),
+        c.sort_vals.get(), c.cell_count.get(), c.flags.get() + 6);
+    ++c.launches;
+    TSF_CUDA(cub::DeviceRadixSort::SortPairs(c.scan_tmp.get(), t_sort, c.sort_keys.get(),
+                                             c.sort_keys_out.get(), c.sort_vals.get(),
+                                             c.sort_vals_out.get(), n, 0, end_bit, c.stream));
+    ++c.launches;
+    k_reorder<<<blocks_for(n), kBlock, 0, c.stream>>>(
+        c.sort_keys_out.get(), c.sort_vals_out.get(), n, c.pos.get(), c.vel.get(), c.tmp4.get(),
+        c.tmp3.get(), c.perm.get(), c.cell_of.get());
+    ++c.launches;
+    swap_buf(c.pos, c.tmp4);
+    swap_buf(c.vel, c.tmp3);
+    refresh_shadow(c);
+    c.sorted = true;
+    c.forces_current = false;
+  }
+  TSF_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.get(), t_scan, c.cell_count.get(),
                                          c.cell_start.get(), int(ncells + 1), c.stream));
   ++c.launches;
-  if (n > 0) {
-    k_cell_fill<<<blocks_for(n), kBlock, 0, c.stream>>>(n, c.cell_of.get(), c.cell_start.get(),
-                                                        c.cell_fill.get(), c.binned.get());
-    ++c.launches;
-  }
 
+  c.tiled = true;
+
+  // ---- skin list in slot indices ----
   int cap = c.skin_list.cap > 0 ? c.skin_list.cap : 32;
   for (int attempt = 0; attempt < 3; ++attempt) {
     c.skin_list.nbr.reserve(std::size_t(cap) * c.npad + 1);
@@ -301,10 +397,10 @@ void list_build(Ctx& c, double cutoff, double skin) {
     TSF_CUDA(cudaMemsetAsync(c.skin_list.cnt.get(), 0, sizeof(int) * c.npad, c.stream));
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 3, 0, sizeof(int), c.stream));
     if (n > 0) {
-      if (cap <= 32) launch_skin<32>(c, g, bc2, cap);
-      else if (cap <= 64) launch_skin<64>(c, g, bc2, cap);
-      else if (cap <= 128) launch_skin<128>(c, g, bc2, cap);
-      else launch_skin<512>(c, g, bc2, cap);
+      if (cap <= 32) launch_skin<32>(c, bc2, cap);
+      else if (cap <= 64) launch_skin<64>(c, bc2, cap);
+      else if (cap <= 128) launch_skin<128>(c, bc2, cap);
+      else launch_skin<512>(c, bc2, cap);
     }
     int mx = 0;
     TSF_CUDA(cudaMemcpyAsync(&mx, c.flags.get() + 3, sizeof(int), cudaMemcpyDeviceToHost,
@@ -323,6 +419,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
   }
   snapshot_reference_positions(c);
   c.short_max_stale = true;
+  c.short_list.valid = false;
 }
 
 void snapshot_reference_positions(Ctx& c) {
@@ -340,9 +437,8 @@ void list_filter(Ctx& c, double r_cut_max, bool apply) {
   if (reread) TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
   if (c.n > 0) {
     k_filter<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
-        c.pos.get(), int(c.n), c.npad, c.box, r_cut_max * r_cut_max, apply ? 1 : 0,
-        c.skin_list.nbr.get(), c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(),
-        c.flags.get() + 4);
+        list_args(c), r_cut_max, r_cut_max * r_cut_max, apply ? 1 : 0, c.skin_list.nbr.get(),
+        c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), c.flags.get() + 4);
     ++c.launches;
   }
   s.valid = true;
