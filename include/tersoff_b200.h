@@ -134,6 +134,26 @@ int64_t tsf_launch_count(const tsf_ctx* ctx);
 int tsf_profile_enable(tsf_ctx* ctx, int on);
 int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset);
 
+/* ---- spatial domain decomposition support ----------------
+ * A rank's context holds its owned atoms as user indices [0, n_owned) and
+ * ghost copies after them, all in the global frame and global box.  Only
+ * owned atoms act as central atoms (energy, virial, and the (i,j,k) terms
+ * they own); forces land on owned and ghost atoms alike and the caller sends
+ * the ghost part back to the owners.  Pointers marked d_ are device pointers
+ * on the context's device; all work is ordered on the context's stream. */
+int tsf_set_stream(tsf_ctx* ctx, void* stream);   /* NULL: back to the context's own */
+int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned);  /* default: all atoms */
+/* d_xyz[m][3] = positions of user atoms d_idx[0..m) */
+int tsf_gather_positions(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, double* d_xyz);
+/* positions of user atoms [lo, lo+m) = d_xyz[m][3] (ghost refresh) */
+int tsf_scatter_positions(tsf_ctx* ctx, int64_t lo, int64_t m, const double* d_xyz);
+/* d_f[m][3] = current forces of user atoms [lo, lo+m) (ghost forces) */
+int tsf_gather_forces(tsf_ctx* ctx, int64_t lo, int64_t m, double* d_f);
+/* forces of user atoms d_idx[0..m) += d_f[m][3] (reverse communication) */
+int tsf_add_forces(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, const double* d_f);
+/* device copies of the latest results: d_out[0] energy, [1..6] virial; forces[n][3] user order */
+int tsf_results_device(tsf_ctx* ctx, double* d_energy_virial, double* d_forces);
+
 /* ---- GPU-resident velocity-Verlet NVE (engine.cpp:142-199) ------------- */
 int tsf_md_set_state(tsf_ctx* ctx, const double* vel, const double* masses /* S */);
 int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel);

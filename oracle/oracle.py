@@ -135,7 +135,7 @@ class Oracle:
         if not os.path.exists(path):
             build()
         L = C.CDLL(path)
-        L.orc_compute_ref.argtypes = [C.c_int64, _dp, _ip, _dp, _up, C.c_int, _dp, _ip, _ip,
+        L.orc_compute_ref.argtypes = [C.c_int64, C.c_int64, _dp, _ip, _dp, _up, C.c_int, _dp, _ip, _ip,
                                       C.POINTER(C.c_double), C.POINTER(C.c_longdouble), _dp,
                                       _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.orc_compute_ref.restype = C.c_int
@@ -206,8 +206,10 @@ class Oracle:
         return bool(self.lib.orc_needs_rebuild(len(xyz), xyz.ravel(), ref, box, per,
                                                float(skin)))
 
-    def compute_ref(self, params: OracleParams, xyz, species, box, periodic, offsets, nbrs):
-        """Returns dict(energy, energy_ld, forces (n,3), virial (6,))."""
+    def compute_ref(self, params: OracleParams, xyz, species, box, periodic, offsets, nbrs,
+                    n_center=None):
+        """Returns dict(energy, energy_ld, forces (n,3), virial (6,)).  With
+        n_center, only atoms [0, n_center) are central atoms."""
         xyz, box, per = self._geom(xyz, box, periodic)
         n = len(xyz)
         f = np.zeros(3 * n)
@@ -215,7 +217,7 @@ class Oracle:
         e = C.c_double(0)
         eld = C.c_longdouble(0)
         bi, bj = C.c_int64(-1), C.c_int64(-1)
-        rc = self.lib.orc_compute_ref(n, xyz.ravel(), np.ascontiguousarray(species, np.int32),
+        rc = self.lib.orc_compute_ref(n, n if n_center is None else n_center, xyz.ravel(), np.ascontiguousarray(species, np.int32),
                                       box, per, params.ns, np.ascontiguousarray(params.rows.ravel()),
                                       np.ascontiguousarray(offsets, np.int32),
                                       np.ascontiguousarray(nbrs, np.int32) if len(nbrs) else

@@ -180,16 +180,18 @@ static void pair_v_terms(double r, double zeta, const double* p, double* energy,
    finite strain derivatives in the tests).  Returns ORC_NUMERIC with
    bad_i / bad_j set on a non-finite pair term (potential_ref.cpp:109-112).
    --------------------------------------------------------------------- */
-int orc_compute_ref(int64_t n, const double* xyz, const int32_t* species,
+int orc_compute_ref(int64_t n, int64_t n_center, const double* xyz, const int32_t* species,
                     const double box[3], const uint8_t per[3], int ns,
                     const double* rows, const int32_t* offsets, const int32_t* nbrs,
                     double* energy, long double* energy_ld, double* forces,
                     double* virial, int64_t* bad_i, int64_t* bad_j) {
+  /* n_center < n: only atoms [0, n_center) act as central atoms (the
+     decomposition tests' owned atoms; the rest are ghost copies). */
   double e = 0.0;
   long double eld = 0.0L;
   long double w[6] = {0, 0, 0, 0, 0, 0};
   memset(forces, 0, sizeof(double) * 3 * (size_t)n);
-  for (int64_t i = 0; i < n; ++i) {
+  for (int64_t i = 0; i < n_center; ++i) {
     const int si = species[i];
     const int32_t s0 = offsets[i], s1 = offsets[i + 1];
     for (int32_t sj_pos = s0; sj_pos < s1; ++sj_pos) {

@@ -79,6 +79,13 @@ PROTOTYPES = [
     ("tsf_launch_count", C.c_int64, [_vp]),
     ("tsf_profile_enable", C.c_int, [_vp, C.c_int]),
     ("tsf_profile_read", C.c_int, [_vp, _vp, _i64p, C.c_int]),
+    ("tsf_set_stream", C.c_int, [_vp, _vp]),
+    ("tsf_set_owned", C.c_int, [_vp, C.c_int64]),
+    ("tsf_gather_positions", C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    ("tsf_scatter_positions", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
+    ("tsf_gather_forces", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
+    ("tsf_add_forces", C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    ("tsf_results_device", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_set_state", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_get_state", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_run", C.c_int, [_vp, C.c_int, C.c_int64, _d, C.c_uint32, C.c_int, _vp, C.c_int64,

@@ -157,6 +157,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
   if (n != c.n) {
     c.n = n;
     c.sorted = false;
+    c.n_owned = -1;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
     c.pos.reserve(nn);
@@ -368,6 +369,7 @@ int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
     if (const char* env = std::getenv("TSF_FUSE_FILTER")) c.fuse_filter = env[0] != '0';
     c.device = device;
     TSF_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.own_stream = c.stream;
     c.flags.reserve(8);
     c.result.reserve(8);
     TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 8 * sizeof(int), c.stream));
@@ -392,9 +394,61 @@ void tsf_destroy(tsf_ctx* ctx) {
   c.pinned = nullptr;
   for (auto& e : c.ev)
     if (e) cudaEventDestroy(e);
-  cudaStream_t s = c.stream;
+  cudaStream_t s = c.own_stream;       // never destroy a caller's stream
   delete ctx;  // DevBufs free themselves
   if (s) cudaStreamDestroy(s);
+}
+
+int tsf_set_stream(tsf_ctx* ctx, void* stream) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
+    c.stream = stream ? static_cast<cudaStream_t>(stream) : c.own_stream;
+  });
+}
+
+int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned) {
+  return guard(&ctx->c, [&] {
+    if (n_owned > ctx->c.n) throw tsf::ConfigError("owned count exceeds the atom count");
+    ctx->c.n_owned = n_owned < 0 ? -1 : n_owned;
+    ctx->c.forces_current = false;
+  });
+}
+
+int tsf_gather_positions(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, double* d_xyz) {
+  return guard(&ctx->c, [&] { tsf::gather_positions(ctx->c, d_idx, m, d_xyz); });
+}
+
+int tsf_scatter_positions(tsf_ctx* ctx, int64_t lo, int64_t m, const double* d_xyz) {
+  return guard(&ctx->c, [&] {
+    if (lo < 0 || lo + m > ctx->c.n) throw tsf::ConfigError("position range out of bounds");
+    tsf::scatter_positions(ctx->c, lo, m, d_xyz);
+  });
+}
+
+int tsf_gather_forces(tsf_ctx* ctx, int64_t lo, int64_t m, double* d_f) {
+  return guard(&ctx->c, [&] {
+    if (lo < 0 || lo + m > ctx->c.n) throw tsf::ConfigError("force range out of bounds");
+    tsf::gather_forces(ctx->c, lo, m, d_f);
+  });
+}
+
+int tsf_add_forces(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, const double* d_f) {
+  return guard(&ctx->c, [&] { tsf::add_forces(ctx->c, d_idx, m, d_f); });
+}
+
+int tsf_results_device(tsf_ctx* ctx, double* d_ev, double* d_forces) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (d_ev)
+      TSF_CUDA(cudaMemcpyAsync(d_ev, c.result.get(), 7 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c.stream));
+    if (d_forces && c.n > 0) {
+      tsf::unpack_forces(c);
+      TSF_CUDA(cudaMemcpyAsync(d_forces, c.forces_user.get(), 3 * c.n * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c.stream));
+    }
+  });
 }
 
 void* tsf_stream(tsf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }

@@ -71,7 +71,10 @@ struct Ctx {
   DevBuf<int> species;         // [n] user order
   std::vector<int> host_species;  // last uploaded species ids
   DevBuf<int> perm;            // [n] slot -> user index
+  DevBuf<int> inv;             // [n] user index -> slot
   bool sorted = false;         // false: perm is the identity (slot == user index)
+  std::int64_t n_owned = -1;   // user atoms [0, n_owned) are centers; -1: all
+  cudaStream_t own_stream = nullptr;
   DevBuf<double4> pos;         // [n] slot order {x, y, z, species}
   DevBuf<float4> posf;         // [n] slot order float shadow for the cutoff pre-tests
   BoxF boxf{};
@@ -145,6 +148,11 @@ void pack_positions(Ctx& c);           // xyz_stage + species (user order) -> po
 void unpack_positions(Ctx& c);         // pos (slots) -> xyz_stage (user order)
 void unpack_forces(Ctx& c);            // forces (slots) -> forces_user
 void unsort(Ctx& c);                   // back to slot == user index (external lists)
+// decomposition support (device pointers, user indices)
+void gather_positions(Ctx& c, const int* d_idx, std::int64_t m, double* d_xyz);
+void scatter_positions(Ctx& c, std::int64_t lo, std::int64_t m, const double* d_xyz);
+void gather_forces(Ctx& c, std::int64_t lo, std::int64_t m, double* d_f);
+void add_forces(Ctx& c, const int* d_idx, std::int64_t m, const double* d_f);
 void refresh_shadow(Ctx& c);           // posf = float(pos)
 void pack_velocities(Ctx& c);          // xyz_stage (user order velocities) -> vel (slots)
 void unpack_velocities(Ctx& c);        // vel (slots) -> xyz_stage (user order)

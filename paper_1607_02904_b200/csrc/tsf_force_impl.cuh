@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "tsf_context.hpp"
@@ -45,7 +46,9 @@ struct ForceArgs {
   Row<R> row0;         // single-species row: read straight from the constant bank
   double cut0;
   const double4* pos;
-  int n_owned;
+  int n_owned;         // slots to cover (all local atoms)
+  const int* perm;     // slot -> user index (nullptr: identity)
+  int center_limit;    // only user atoms below this act as centers (ghosts above)
   int npad;
   Box box;
   const int* nbr;      // short list (unfused) or output short list (fused)
@@ -220,6 +223,14 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
       if (work >= ntiles) break;       // block-uniform
       i = work * kAtomsPerBlock + tid / G;
       active = i < a.n_owned;
+      // ghost copies (decomposition) receive forces but are not centers
+      if (active && (a.perm ? a.perm[i] : i) >= a.center_limit) {
+        if (DET && gl == 0) {
+          Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+          f[0] = f[1] = f[2] = Acc(0);
+        }
+        active = false;
+      }
     }
 
     const double4 pi = a.pos[active ? i : 0];
@@ -573,16 +584,20 @@ int ceil_div(std::int64_t a, int b) { return int((a + b - 1) / b); }
 // Persistent grid: resident blocks per SM x SM count, capped by the tile count.
 template <typename K>
 int persistent_blocks(K kernel, int tiles) {
-  static std::map<const void*, int> cache;
+  static std::map<const void*, int> cache;   // contexts may live on several threads
+  static std::mutex mu;
   const void* key = reinterpret_cast<const void*>(kernel);
-  auto it = cache.find(key);
   int per_sm;
-  if (it == cache.end()) {
-    TSF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
-    per_sm = std::max(1, per_sm);
-    cache[key] = per_sm;
-  } else {
-    per_sm = it->second;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      TSF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+      per_sm = std::max(1, per_sm);
+      cache[key] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
   }
   int dev = 0, sms = 148;
   TSF_CUDA(cudaGetDevice(&dev));
@@ -649,6 +664,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.cut0 = c.params.entry(0, 0, 0).cutoff() * c.params.entry(0, 0, 0).cutoff();
   a.pos = c.pos.get();
   a.n_owned = int(c.n);
+  a.perm = c.sorted ? c.perm.get() : nullptr;
+  a.center_limit = int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
   a.npad = npad;
   a.box = c.box;
   // fused: the kernel filters the skin list itself and writes the short list

@@ -71,6 +71,54 @@ __global__ void k_unsort_pos(const double4* __restrict__ in, const int* __restri
   out[perm[s]] = in[s];
 }
 
+__device__ __forceinline__ int slot_of(const int* __restrict__ inv, int u) {
+  return inv ? inv[u] : u;
+}
+
+__global__ void k_gather_pos(const double4* __restrict__ pos, const int* __restrict__ inv,
+                             const int* __restrict__ idx, int m, double* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const double4 p = pos[slot_of(inv, idx[q])];
+  out[3 * q] = p.x;
+  out[3 * q + 1] = p.y;
+  out[3 * q + 2] = p.z;
+}
+
+__global__ void k_scatter_pos(double4* __restrict__ pos, float4* __restrict__ posf,
+                              int* __restrict__ cmax, const int* __restrict__ inv,
+                              const int* __restrict__ species, int lo, int m,
+                              const double* __restrict__ in) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const int s = slot_of(inv, lo + q);
+  const double4 p = make_double4(in[3 * q], in[3 * q + 1], in[3 * q + 2], double(species[lo + q]));
+  pos[s] = p;
+  posf[s] = shadow(p);
+  track_coord_max(cmax, p);
+}
+
+__global__ void k_gather_f(const double* __restrict__ f, const int* __restrict__ inv, int lo,
+                           int m, double* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const int s = slot_of(inv, lo + q);
+  out[3 * q] = f[3 * s];
+  out[3 * q + 1] = f[3 * s + 1];
+  out[3 * q + 2] = f[3 * s + 2];
+}
+
+// indices are unique per call (one owner copy per ghost), so no atomics
+__global__ void k_add_f(double* __restrict__ f, const int* __restrict__ inv,
+                        const int* __restrict__ idx, int m, const double* __restrict__ in) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const int s = slot_of(inv, idx[q]);
+  f[3 * s] += in[3 * q];
+  f[3 * s + 1] += in[3 * q + 1];
+  f[3 * s + 2] += in[3 * q + 2];
+}
+
 // wrap_1d (box.hpp:41-46)
 __device__ __forceinline__ double wrap(double x, double len) {
   x = __dsub_rn(x, __dmul_rn(len, floor(__ddiv_rn(x, len))));
@@ -151,8 +199,38 @@ Masses masses_of(const Ctx& c) {
 }
 
 const int* perm_of(const Ctx& c) { return c.sorted ? c.perm.get() : nullptr; }
+const int* inv_of(const Ctx& c) { return c.sorted ? c.inv.get() : nullptr; }
 
 }  // namespace
+
+void gather_positions(Ctx& c, const int* d_idx, std::int64_t m, double* d_xyz) {
+  if (m <= 0) return;
+  k_gather_pos<<<blocks_for(m), kBlock, 0, c.stream>>>(c.pos.get(), inv_of(c), d_idx, int(m),
+                                                       d_xyz);
+  ++c.launches;
+}
+
+void scatter_positions(Ctx& c, std::int64_t lo, std::int64_t m, const double* d_xyz) {
+  if (m <= 0) return;
+  k_scatter_pos<<<blocks_for(m), kBlock, 0, c.stream>>>(c.pos.get(), c.posf.get(),
+                                                        c.flags.get() + 5, inv_of(c),
+                                                        c.species.get(), int(lo), int(m), d_xyz);
+  ++c.launches;
+  c.forces_current = false;
+}
+
+void gather_forces(Ctx& c, std::int64_t lo, std::int64_t m, double* d_f) {
+  if (m <= 0) return;
+  k_gather_f<<<blocks_for(m), kBlock, 0, c.stream>>>(c.forces.get(), inv_of(c), int(lo), int(m),
+                                                     d_f);
+  ++c.launches;
+}
+
+void add_forces(Ctx& c, const int* d_idx, std::int64_t m, const double* d_f) {
+  if (m <= 0) return;
+  k_add_f<<<blocks_for(m), kBlock, 0, c.stream>>>(c.forces.get(), inv_of(c), d_idx, int(m), d_f);
+  ++c.launches;
+}
 
 void pack_positions(Ctx& c) {
   if (c.n == 0) return;

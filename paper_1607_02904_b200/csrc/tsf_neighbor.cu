@@ -73,7 +73,7 @@ __global__ void k_reorder(const unsigned long long* __restrict__ keys,
                           const int* __restrict__ src, int n, const double4* __restrict__ pos_in,
                           const double* __restrict__ vel_in, double4* __restrict__ pos_out,
                           double* __restrict__ vel_out, int* __restrict__ perm,
-                          int* __restrict__ cell_of) {
+                          int* __restrict__ inv, int* __restrict__ cell_of) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int s = src[t];
@@ -82,7 +82,9 @@ __global__ void k_reorder(const unsigned long long* __restrict__ keys,
   vel_out[3 * t] = vel_in[3 * s];
   vel_out[3 * t + 1] = vel_in[3 * s + 1];
   vel_out[3 * t + 2] = vel_in[3 * s + 2];
-  perm[t] = int(k & 0xffffffffull);
+  const int user = int(k & 0xffffffffull);
+  perm[t] = user;
+  inv[user] = t;
   cell_of[t] = int(k >> 32);
 }
 
@@ -351,6 +353,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
   c.sort_vals.reserve(nn);
   c.sort_vals_out.reserve(nn);
   c.perm.reserve(nn);
+  c.inv.reserve(nn);
   c.tmp4.reserve(nn);
   c.tmp3.reserve(3 * nn);
   const int end_bit = 32 + bits_for(ncells);
@@ -375,7 +378,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
     ++c.launches;
     k_reorder<<<blocks_for(n), kBlock, 0, c.stream>>>(
         c.sort_keys_out.get(), c.sort_vals_out.get(), n, c.pos.get(), c.vel.get(), c.tmp4.get(),
-        c.tmp3.get(), c.perm.get(), c.cell_of.get());
+        c.tmp3.get(), c.perm.get(), c.inv.get(), c.cell_of.get());
     ++c.launches;
     swap_buf(c.pos, c.tmp4);
     swap_buf(c.vel, c.tmp3);

@@ -1,0 +1,262 @@
+"""x-slab spatial domain decomposition of the Tersoff path.
+
+The reference has no distribution at all; this is the B200-native
+multi-GPU form of the paper's LAMMPS runs (Fig. 9): one process per
+GPU, torch.distributed (NCCL over NVLink) for the two exchange steps a
+many-body force evaluation needs:
+
+  forward  ghost positions: atoms within r_cut_max + skin of a slab face are
+           copied to the neighbour slab every step;
+  reverse  ghost forces: the (i, j, k) terms of an owned centre put forces on
+           ghosts; those go back to the owners and are added (Newton's third
+           law across the face).
+
+Everything stays in the GLOBAL frame and the global periodic box: ghosts keep
+their owners' wrapped coordinates, so every displacement is the reference's
+minimum image bit for bit, and a rank's neighbour lists are exactly the
+global lists restricted to its owned atoms.  Only owned atoms act as centres
+(`tsf_set_owned`), so each (i, j, k) term is computed once, by the owner of i.
+
+Engines: `GpuEngine` (libtersoff_b200.so, device tensors, NCCL) is the
+product.  The same `Decomposition` logic is exercised on CPU with gloo and an
+oracle engine in tests/test_parallel.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .api import Context, ConfigError, _check
+
+TAG_FWD_LEFT, TAG_FWD_RIGHT, TAG_REV_RIGHT, TAG_REV_LEFT = 11, 12, 13, 14
+
+
+@dataclass
+class Slab:
+    rank: int
+    world: int
+    length: float          # box length along x
+    halo: float            # r_cut_max + skin
+
+    @property
+    def width(self) -> float:
+        return self.length / self.world
+
+    @property
+    def lo(self) -> float:
+        return self.rank * self.width
+
+    @property
+    def hi(self) -> float:
+        return (self.rank + 1) * self.width
+
+    def owner(self, x: np.ndarray) -> np.ndarray:
+        """Owning rank of wrapped x coordinates."""
+        xw = np.mod(x, self.length)
+        return np.minimum((xw / self.width).astype(np.int64), self.world - 1)
+
+    def near_left(self, x: np.ndarray) -> np.ndarray:
+        """Owned atoms the left neighbour needs: within halo of the left face."""
+        return np.mod(x - self.lo, self.length) <= self.halo
+
+    def near_right(self, x: np.ndarray) -> np.ndarray:
+        return np.mod(self.hi - x, self.length) <= self.halo
+
+
+class GpuEngine:
+    """Device-resident engine: one context per rank on the caller's stream."""
+
+    def __init__(self, params, device: int):
+        self.ctx = Context(params, device)
+        self.device = torch.device("cuda", device)
+        self._lib = L.lib()
+        self.ctx._ok(self._lib.tsf_set_stream(self.ctx._h,
+                                              C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+
+    def _p(self, t: torch.Tensor):
+        return C.c_void_p(t.data_ptr())
+
+    def load(self, xyz: np.ndarray, species: np.ndarray, box, periodic, n_owned: int):
+        self.ctx.set_system(xyz, species, box, periodic)
+        self.ctx._ok(self._lib.tsf_set_owned(self.ctx._h, n_owned))
+
+    def build(self, cutoff: float, skin: float):
+        self.ctx.build_neighbor_list(cutoff, skin)
+
+    def gather_positions(self, idx: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((len(idx), 3), dtype=torch.float64, device=self.device)
+        if len(idx):
+            self.ctx._ok(self._lib.tsf_gather_positions(self.ctx._h, self._p(idx), len(idx),
+                                                        self._p(out)))
+        return out
+
+    def scatter_positions(self, lo: int, xyz: torch.Tensor):
+        if len(xyz):
+            self.ctx._ok(self._lib.tsf_scatter_positions(self.ctx._h, lo, len(xyz), self._p(xyz)))
+
+    def compute(self, precision: str = "double", deterministic: bool = False):
+        self.ctx.compute(precision, deterministic=deterministic, energy=False, forces=False,
+                         virial=False)
+
+    def ghost_forces(self, lo: int, m: int) -> torch.Tensor:
+        out = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+        if m:
+            self.ctx._ok(self._lib.tsf_gather_forces(self.ctx._h, lo, m, self._p(out)))
+        return out
+
+    def add_forces(self, idx: torch.Tensor, f: torch.Tensor):
+        if len(idx):
+            self.ctx._ok(self._lib.tsf_add_forces(self.ctx._h, self._p(idx), len(idx), self._p(f)))
+
+    def results(self):
+        ev = torch.empty(7, dtype=torch.float64, device=self.device)
+        f = torch.empty((self.ctx.n, 3), dtype=torch.float64, device=self.device)
+        self.ctx._ok(self._lib.tsf_results_device(self.ctx._h, self._p(ev), self._p(f)))
+        return ev, f
+
+
+class Decomposition:
+    """One rank's view: owned atoms (global ids), ghost blocks, send lists."""
+
+    def __init__(self, engine, box, periodic, halo: float, group=None):
+        self.engine = engine
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.box = np.asarray(box, np.float64)
+        self.periodic = np.asarray(periodic, np.uint8)
+        if self.world > 1:
+            if not self.periodic[0]:
+                raise ConfigError("slab decomposition needs a periodic x axis")
+            if self.box[0] / self.world < 2.0 * halo:
+                raise ConfigError(f"{self.world} slabs of {self.box[0] / self.world:.3f} A are "
+                                  f"thinner than 2 x halo = {2 * halo:.3f} A")
+        self.slab = Slab(self.rank, self.world, float(self.box[0]), float(halo))
+        self.left = (self.rank - 1) % self.world
+        self.right = (self.rank + 1) % self.world
+
+    # ---- exchange helpers ------------------------------------------------
+    def _device(self):
+        return getattr(self.engine, "device", torch.device("cpu"))
+
+    def _exchange(self, sends, recvs):
+        """sends: [(tensor, dst, tag)], recvs: [(tensor, src, tag)] in a fixed
+        order on every rank (NCCL matches per pair in issue order, gloo by tag)."""
+        ops = [dist.P2POp(dist.isend, t, d, self.group, tag) for t, d, tag in sends if t.numel()]
+        ops += [dist.P2POp(dist.irecv, t, s, self.group, tag) for t, s, tag in recvs if t.numel()]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def _swap_counts(self, n_left: int, n_right: int):
+        dev = self._device()
+        send_l = torch.tensor([n_left], dtype=torch.int64, device=dev)
+        send_r = torch.tensor([n_right], dtype=torch.int64, device=dev)
+        from_r = torch.zeros(1, dtype=torch.int64, device=dev)
+        from_l = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
+                       [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+        return int(from_l.item()), int(from_r.item())
+
+    # ---- setup at a (re)build -------------------------------------------
+    def setup(self, gid: np.ndarray, xyz: np.ndarray, species: np.ndarray, cutoff: float,
+              skin: float):
+        """gid/xyz/species: this rank's owned atoms (global ids, global frame)."""
+        order = np.argsort(gid, kind="stable")
+        self.gid = np.ascontiguousarray(gid[order], np.int64)
+        xyz = np.ascontiguousarray(xyz[order], np.float64)
+        species = np.ascontiguousarray(species[order], np.int32)
+        self.n_owned = len(self.gid)
+        dev = self._device()
+        if self.world == 1:
+            self.send_left = self.send_right = np.zeros(0, np.int64)
+            self.n_gl = self.n_gr = 0
+            gxyz = np.zeros((0, 3))
+            gsp = np.zeros(0, np.int32)
+            self.ghost_gid = np.zeros(0, np.int64)
+        else:
+            self.send_left = np.nonzero(self.slab.near_left(xyz[:, 0]))[0]
+            self.send_right = np.nonzero(self.slab.near_right(xyz[:, 0]))[0]
+            self.n_gl, self.n_gr = self._swap_counts(len(self.send_left), len(self.send_right))
+            # ghost payload: global id, species, xyz (as float64 rows)
+            def pack(idx):
+                return torch.from_numpy(np.column_stack([self.gid[idx].astype(np.float64),
+                                                         species[idx].astype(np.float64),
+                                                         xyz[idx]])).to(dev)
+            from_l = torch.zeros((self.n_gl, 5), dtype=torch.float64, device=dev)
+            from_r = torch.zeros((self.n_gr, 5), dtype=torch.float64, device=dev)
+            self._exchange([(pack(self.send_left), self.left, TAG_FWD_LEFT),
+                            (pack(self.send_right), self.right, TAG_FWD_RIGHT)],
+                           [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+            ghosts = torch.cat([from_l, from_r]).cpu().numpy()
+            self.ghost_gid = ghosts[:, 0].astype(np.int64)
+            gsp = ghosts[:, 1].astype(np.int32)
+            gxyz = np.ascontiguousarray(ghosts[:, 2:5])
+        self.local_xyz = np.concatenate([xyz, gxyz])
+        self.local_species = np.concatenate([species, gsp]).astype(np.int32)
+        self.engine.load(self.local_xyz, self.local_species, self.box, self.periodic,
+                         self.n_owned)
+        self.engine.build(cutoff, skin)
+        self.t_send_left = torch.from_numpy(self.send_left.astype(np.int32)).to(dev)
+        self.t_send_right = torch.from_numpy(self.send_right.astype(np.int32)).to(dev)
+
+    # ---- one force evaluation ------------------------------------------
+    def forward(self):
+        """Refresh ghost positions from their owners."""
+        if self.world == 1:
+            return
+        dev = self._device()
+        send_l = self.engine.gather_positions(self.t_send_left)
+        send_r = self.engine.gather_positions(self.t_send_right)
+        from_l = torch.empty((self.n_gl, 3), dtype=torch.float64, device=dev)
+        from_r = torch.empty((self.n_gr, 3), dtype=torch.float64, device=dev)
+        self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
+                       [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+        self.engine.scatter_positions(self.n_owned, from_l)
+        self.engine.scatter_positions(self.n_owned + self.n_gl, from_r)
+
+    def reverse(self):
+        """Send ghost forces home and add them to the owners' forces."""
+        if self.world == 1:
+            return
+        dev = self._device()
+        f_gl = self.engine.ghost_forces(self.n_owned, self.n_gl)
+        f_gr = self.engine.ghost_forces(self.n_owned + self.n_gl, self.n_gr)
+        to_l = torch.empty((len(self.send_left), 3), dtype=torch.float64, device=dev)
+        to_r = torch.empty((len(self.send_right), 3), dtype=torch.float64, device=dev)
+        # my right ghosts are the right neighbour's send_left; my left ghosts its send_right
+        self._exchange([(f_gr, self.right, TAG_REV_RIGHT), (f_gl, self.left, TAG_REV_LEFT)],
+                       [(to_l, self.left, TAG_REV_RIGHT), (to_r, self.right, TAG_REV_LEFT)])
+        self.engine.add_forces(self.t_send_left, to_l)
+        self.engine.add_forces(self.t_send_right, to_r)
+
+    def evaluate(self, precision: str = "double", deterministic: bool = False):
+        self.forward()
+        self.engine.compute(precision, deterministic)
+        self.reverse()
+
+    def gather_results(self, total_atoms: int):
+        """Energy/virial summed over ranks and global-order forces on rank 0
+        (a check/report path, not the per-step loop)."""
+        ev, f = self.engine.results()
+        if self.world > 1:
+            dist.all_reduce(ev, group=self.group)
+        owned = f[: self.n_owned].double().cpu().numpy()
+        parts = [None] * self.world if self.world > 1 else [(self.gid, owned)]
+        if self.world > 1:
+            dist.all_gather_object(parts, (self.gid, owned), group=self.group)
+        forces = np.zeros((total_atoms, 3))
+        for gid, fo in parts:
+            forces[gid] = fo
+        e = ev.cpu().numpy()
+        return float(e[0]), forces, e[1:7].copy()
+
+
+def partition(xyz: np.ndarray, box, world: int, rank: int, halo: float) -> np.ndarray:
+    """Global ids owned by `rank` (x slabs of equal width)."""
+    return np.nonzero(Slab(rank, world, float(box[0]), halo).owner(xyz[:, 0]) == rank)[0]

@@ -1,0 +1,148 @@
+"""Device side of the slab decomposition on one B200.
+
+* `tsf_set_owned`: only owned atoms act as centres; forces land on ghosts
+  too — checked against the oracle's n_center evaluation;
+* gather/scatter of positions and forces by user index;
+* two emulated ranks in one process (threads, one context each, exchanging
+  through host mailboxes after a stream sync — no kernel waits on another
+  rank's kernel): the decomposed result equals the single-context result.
+"""
+import queue
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import systems
+
+pytestmark = pytest.mark.gpu
+
+
+def test_owned_centres_match_oracle(tb, oracle):
+    from oracle.oracle import parse_param_text
+    c = systems.perturbed(tb, 4, 0.15, 17, skin=0.5)
+    n = len(c.xyz)
+    rng = np.random.default_rng(3)
+    order = rng.permutation(n)               # owned = first 300 of a shuffled order
+    xyz, sp = c.xyz[order], c.species[order]
+    n_owned = 300
+    op = parse_param_text(c.params_text)
+    off, nb = oracle.build_neighbor_list(xyz, c.box, c.periodic, op.r_cut_max, c.skin)
+    ref = oracle.compute_ref(op, xyz, sp, c.box, c.periodic, off, nb, n_center=n_owned)
+    params = tb.builtin_silicon()
+    ctx = tb.Context(params, 0)
+    ctx.set_system(xyz, sp, c.box, c.periodic)
+    ctx.build_neighbor_list(params.r_cut_max, c.skin)
+    from paper_1607_02904_b200 import _lib as L
+    ctx._ok(L.lib().tsf_set_owned(ctx._h, n_owned))
+    for det in (True, False):
+        for prec, etol, ftol in (("double", 1e-12, 1e-10), ("mixed", 1e-6, 1e-4)):
+            e, f, w = ctx.compute(prec, deterministic=det)
+            assert abs(e - ref["energy"]) <= etol * abs(ref["energy"])
+            assert np.abs(f - ref["forces"]).max() <= ftol * max(1, np.abs(ref["forces"]).max())
+
+
+def test_gather_scatter_add(tb):
+    import ctypes as C
+    from paper_1607_02904_b200 import _lib as L
+    c = systems.perturbed(tb, 3, 0.1, 4, skin=0.5)
+    params = tb.builtin_silicon()
+    ctx = tb.Context(params, 0)
+    ctx.set_system(c.xyz, c.species, c.box, c.periodic)
+    ctx.build_neighbor_list(params.r_cut_max, c.skin)   # cell-sorts the slots
+    lib = L.lib()
+    dev = torch.device("cuda", 0)
+    idx = torch.tensor([5, 0, 17, 200], dtype=torch.int32, device=dev)
+    out = torch.empty((4, 3), dtype=torch.float64, device=dev)
+    ctx._ok(lib.tsf_gather_positions(ctx._h, C.c_void_p(idx.data_ptr()), 4,
+                                     C.c_void_p(out.data_ptr())))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), c.xyz[[5, 0, 17, 200]])
+    new = torch.from_numpy(c.xyz[10:14] + 0.01).to(dev)
+    ctx._ok(lib.tsf_scatter_positions(ctx._h, 10, 4, C.c_void_p(new.data_ptr())))
+    np.testing.assert_array_equal(ctx.get_positions()[10:14], c.xyz[10:14] + 0.01)
+    e, f, _ = ctx.compute("double", deterministic=True)
+    got = torch.empty((3, 3), dtype=torch.float64, device=dev)
+    ctx._ok(lib.tsf_gather_forces(ctx._h, 20, 3, C.c_void_p(got.data_ptr())))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), f[20:23])
+    add = torch.ones((4, 3), dtype=torch.float64, device=dev)
+    ctx._ok(lib.tsf_add_forces(ctx._h, C.c_void_p(idx.data_ptr()), 4, C.c_void_p(add.data_ptr())))
+    ev = torch.empty(7, dtype=torch.float64, device=dev)
+    fu = torch.empty((len(c.xyz), 3), dtype=torch.float64, device=dev)
+    ctx._ok(lib.tsf_results_device(ctx._h, C.c_void_p(ev.data_ptr()), C.c_void_p(fu.data_ptr())))
+    torch.cuda.synchronize()
+    expect = f.copy()
+    expect[[5, 0, 17, 200]] += 1.0
+    np.testing.assert_array_equal(fu.cpu().numpy(), expect)
+    assert ev[0].item() == e
+
+
+class _Mailbox:
+    def __init__(self):
+        self.q = {}
+        self.lock = threading.Lock()
+
+    def box(self, src, dst, tag):
+        with self.lock:
+            return self.q.setdefault((src, dst, tag), queue.Queue())
+
+
+def _emulated(tb, mail, rank, world, c, out):
+    """One emulated rank: Decomposition with a mailbox exchange (host copies)."""
+    from paper_1607_02904_b200 import parallel as P
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        eng = P.GpuEngine(tb.builtin_silicon(), 0)
+        halo = 3.2 + c.skin
+        dec = P.Decomposition.__new__(P.Decomposition)
+        dec.engine, dec.group = eng, None
+        dec.rank, dec.world = rank, world
+        dec.box, dec.periodic = np.asarray(c.box), np.asarray(c.periodic, np.uint8)
+        dec.slab = P.Slab(rank, world, float(c.box[0]), halo)
+        dec.left, dec.right = (rank - 1) % world, (rank + 1) % world
+
+        def exchange(sends, recvs):
+            torch.cuda.current_stream().synchronize()
+            for t, dst, tag in sends:
+                mail.box(rank, dst, tag).put(t.cpu().clone())
+            for t, src, tag in recvs:
+                t.copy_(mail.box(src, rank, tag).get(timeout=60).to(t.device))
+            torch.cuda.current_stream().synchronize()
+        dec._exchange = exchange
+        gid = P.partition(c.xyz, c.box, world, rank, halo)
+        dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
+        dec.evaluate("double", deterministic=True)
+        ev, f = eng.results()
+        torch.cuda.current_stream().synchronize()
+        out[rank] = (dec.gid, f[: dec.n_owned].cpu().numpy(), ev.cpu().numpy(),
+                     len(dec.ghost_gid))
+
+
+def test_two_emulated_ranks_match_one_context(tb):
+    c = systems.perturbed(tb, 5, 0.12, 21, skin=0.5)
+    params = tb.builtin_silicon()
+    ctx = tb.Context(params, 0)
+    ctx.set_system(c.xyz, c.species, c.box, c.periodic)
+    ctx.build_neighbor_list(params.r_cut_max, c.skin)
+    e1, f1, w1 = ctx.compute("double", deterministic=True)
+    mail, out = _Mailbox(), {}
+    threads = [threading.Thread(target=_emulated, args=(tb, mail, r, 2, c, out)) for r in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+    assert len(out) == 2
+    f = np.zeros_like(f1)
+    e = 0.0
+    w = np.zeros(6)
+    for gid, fo, ev, nghost in out.values():
+        assert nghost > 0
+        f[gid] = fo
+        e += ev[0]
+        w += ev[1:7]
+    assert abs(e - e1) <= 1e-12 * abs(e1)
+    assert np.abs(f - f1).max() <= 1e-10
+    assert np.abs(w - w1).max() <= 1e-10 * np.abs(w1).max()

@@ -1,0 +1,124 @@
+"""Multi-rank decomposition logic on CPU: world_size 2 and 3 over gloo.
+
+The product's `paper_1607_02904_b200.parallel.Decomposition` (slab ownership,
+ghost selection, forward position / reverse force exchange, result gather)
+runs unchanged; the engine is the CPU oracle restricted to owned centres
+(`n_center`).  The decomposed energy, forces and virial must equal the
+single-process oracle: the x-slab split in the global frame is exact up to
+summation order.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import systems
+
+
+class OracleEngine:
+    """Engine interface of parallel.GpuEngine, backed by the CPU oracle."""
+
+    def __init__(self, oracle, params_text):
+        from oracle.oracle import parse_param_text
+        self.oracle = oracle
+        self.op = parse_param_text(params_text)
+        self.device = torch.device("cpu")
+
+    def load(self, xyz, species, box, periodic, n_owned):
+        self.xyz = np.array(xyz, np.float64)
+        self.species = np.asarray(species, np.int32)
+        self.box, self.per, self.n_owned = np.asarray(box), np.asarray(periodic), n_owned
+
+    def build(self, cutoff, skin):
+        self.off, self.nb = self.oracle.build_neighbor_list(self.xyz, self.box, self.per, cutoff,
+                                                            skin)
+
+    def gather_positions(self, idx):
+        return torch.from_numpy(self.xyz[idx.numpy()].copy())
+
+    def scatter_positions(self, lo, t):
+        self.xyz[lo:lo + len(t)] = t.numpy()
+
+    def compute(self, precision="double", deterministic=False):
+        r = self.oracle.compute_ref(self.op, self.xyz, self.species, self.box, self.per, self.off,
+                                    self.nb, n_center=self.n_owned)
+        self.f = r["forces"].copy()
+        self.ev = np.concatenate([[r["energy"]], r["virial"]])
+
+    def ghost_forces(self, lo, m):
+        return torch.from_numpy(self.f[lo:lo + m].copy())
+
+    def add_forces(self, idx, t):
+        self.f[idx.numpy()] += t.numpy()
+
+    def results(self):
+        return torch.from_numpy(self.ev.copy()), torch.from_numpy(self.f.copy())
+
+
+def _case(cells):
+    import paper_1607_02904_b200 as tb
+    return systems.perturbed(tb, cells, 0.15, 17, skin=0.5)
+
+
+def _worker(rank, world, port, cells, shift, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_1607_02904_b200.parallel import Decomposition, partition
+        c = _case(cells)
+        halo = 3.2 + c.skin
+        gid = partition(c.xyz, c.box, world, rank, halo)
+        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo)
+        dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
+        if shift is not None:
+            # move owned atoms a little: the forward exchange must refresh ghosts
+            moved = np.mod(c.xyz + shift, c.box)
+            dec.engine.scatter_positions(0, torch.from_numpy(moved[dec.gid]))
+        dec.evaluate()
+        e, f, w = dec.gather_results(len(c.xyz))
+        if rank == 0:
+            np.savez(out_path, e=e, f=f, w=w, n_owned=dec.n_owned, n_ghost=len(dec.ghost_gid))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world,cells,shifted", [(2, 4, False), (2, 4, True), (3, 5, False)])
+def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted):
+    from oracle.oracle import parse_param_text
+    c = _case(cells)
+    shift = np.array([0.03, -0.02, 0.01]) if shifted else None
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out), nprocs=world, join=True)
+    res = np.load(out)
+    op = parse_param_text(c.params_text)
+    off, nb = oracle.build_neighbor_list(c.xyz, c.box, c.periodic, op.r_cut_max, c.skin)
+    xyz = np.mod(c.xyz + shift, c.box) if shifted else c.xyz
+    ref = oracle.compute_ref(op, xyz, c.species, c.box, c.periodic, off, nb)
+    assert res["n_ghost"] > 0
+    assert abs(res["e"] - ref["energy"]) <= 1e-12 * abs(ref["energy"])
+    assert np.abs(res["f"] - ref["forces"]).max() <= 1e-10
+    assert np.abs(res["w"] - ref["virial"]).max() <= 1e-10 * np.abs(ref["virial"]).max()
+
+
+def test_slab_geometry_guards():
+    from paper_1607_02904_b200.parallel import Slab
+    s = Slab(rank=1, world=4, length=40.0, halo=3.0)
+    assert (s.lo, s.hi) == (10.0, 20.0)
+    x = np.array([10.0, 12.9, 13.1, 17.0, 19.99, 39.9])
+    assert s.near_left(x).tolist() == [True, True, False, False, False, False]
+    assert s.near_right(x).tolist() == [False, False, False, True, True, False]
+    assert Slab(0, 4, 40.0, 3.0).owner(np.array([-0.5, 0.0, 9.99, 10.0, 39.99, 40.0])).tolist() == \
+        [3, 0, 0, 1, 3, 0]
