@@ -1,0 +1,73 @@
+"""GPU-resident velocity-Verlet NVE (tsf_md_run; engine.cpp:142-199) on a B200.
+
+* short trajectories follow the reference Engine (oracle/_ref) step for step;
+* energy conservation and momentum (acceptance criterion 4's bars);
+* the tersoffmd-shaped run_nve surface (tests/python/test_smoke.py:68-82).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _lattice(tb, cells, T, seed):
+    s = tb.make_diamond_lattice(cells, cells, cells)
+    tb.init_velocities(s, T, seed)
+    return s
+
+
+def test_trajectory_follows_reference_engine(tb, reference):
+    R = reference
+    from oracle.oracle import SI_TEXT
+    s = _lattice(tb, 4, 1600.0, 12345)
+    steps = 60
+    h = R.diamond_lattice(4, 4, 4)
+    R.init_velocities(h, 1600.0, 12345)
+    ph = R.params(SI_TEXT)
+    rep_ref = R.run_nve(h, ph, steps, dt=0.001, skin=1.0, scheme="ref", precision="ref",
+                        thermo_every=steps)
+    xr, vr, *_ = R.system_arrays(rep_ref["final"])
+    rep = tb.run_nve(s, tb.builtin_silicon(), steps, dt=0.001, skin=1.0, thermo_every=steps,
+                     deterministic=True)
+    fin = rep["system"]
+    dx = fin.positions - xr
+    dx -= fin.box.lengths * np.round(dx / fin.box.lengths)
+    assert np.abs(dx).max() < 1e-8
+    assert np.abs(fin.velocities - vr).max() < 1e-6
+    e0, e1 = rep["samples"][0]["etot_eV"], rep["samples"][-1]["etot_eV"]
+    assert abs(e0 - rep_ref["etot_first"]) <= 1e-12 * abs(e0)
+    assert abs(e1 - rep_ref["etot_last"]) <= 1e-9 * abs(e1)
+    assert rep["neighbor_rebuilds"] == rep_ref["rebuilds"]
+
+
+@pytest.mark.parametrize("precision,tol", [("double", 1e-4), ("mixed", 1e-4), ("single", 2e-4)])
+def test_nve_energy_conservation(tb, precision, tol):
+    s = _lattice(tb, 4, 300.0, 2027)
+    rep = tb.run_nve(s, tb.builtin_silicon(), 2000, dt=0.001, skin=1.0, precision=precision,
+                     thermo_every=100)
+    e = np.array([x["etot_eV"] for x in rep["samples"]])
+    assert np.abs(e - e[0]).max() / abs(e[0]) < tol
+    fin = rep["system"]
+    assert np.abs(fin.forces.sum(axis=0)).max() < (1e-10 if precision == "double" else 1e-6)
+    m = np.asarray(fin.species_masses)[fin.species]
+    p = (fin.velocities * m[:, None]).sum(axis=0)
+    # float per-atom partials leave |sum F| ~ 1e-7 eV/A: a momentum walk of
+    # ~1e-4 (g/mol)(A/ps) over 2000 steps, i.e. 1e-8 A/ps of centre-of-mass drift
+    assert np.abs(p).max() < (1e-8 if precision == "double" else 1e-3)
+
+
+def test_run_nve_surface(tb):
+    """tests/python/test_smoke.py:68-82 against the GPU engine."""
+    params = tb.builtin_silicon()
+    s = tb.make_diamond_lattice(2, 2, 2)
+    tb.init_velocities(s, 300.0, 11)
+    rep = tb.run_nve(s, params, steps=50, dt=0.001, thermo_every=10)
+    samples = rep["samples"]
+    assert [x["step"] for x in samples] == [0, 10, 20, 30, 40, 50]
+    e0 = samples[0]["etot_eV"]
+    assert max(abs(x["etot_eV"] - e0) for x in samples) <= 1e-4 * abs(e0)
+    assert rep["width"] in (1, 4, 8, 16)
+    assert rep["precision"] == "opt-d"
+    assert rep["csv"].startswith("step,time_ps,temp_K,pe_eV,ke_eV,etot_eV")
+    assert rep["system"].natoms == 64
+    assert abs(tb.temperature(s) - 300.0) <= 1e-9     # input untouched
