@@ -49,10 +49,6 @@ struct Ctx {
   Params params;
   bool has_potential = true;   // false: list-only context (tsf_create with NULL params)
   bool hoist_ramp = true;
-  // Filter inside the force kernel (env TSF_FUSE_FILTER=1).  Off by default:
-  // measured slower at 2M atoms (0.90 vs 0.66 ms, f64) because the gather
-  // latency lands in the low-occupancy FP64 kernel (profiles/r01).
-  bool fuse_filter = false;
   std::string err;
   std::int64_t launches = 0;
 

@@ -23,10 +23,13 @@
 //     atom's incoming slots in list order — bitwise reproducible;
 //   * energy and virial (W_ab = sum_l d_a P_b) are reduced per block into a
 //     partials array and summed in fixed order: deterministic in both modes.
-// The grid is persistent (a few blocks per SM striding over atom tiles): one
-// parameter load and one block reduction per block.  Atoms whose short count
-// exceeds G are queued and processed by the same code with G = 32 (one warp
-// per atom) in a second launch that exits at once when the queue is empty.
+// The grid is persistent (occupancy x 148 blocks striding over atom tiles)
+// and software-pipelined: while tile k computes, the positions of tile k+1
+// and the list entries of tile k+2 are already in flight (the dependent
+// count -> index -> position loads were 35% of the stall samples, ncu).
+// Atoms whose short count exceeds G are queued and processed by the same code
+// with G = 32 (one warp per atom) in a second launch that exits at once when
+// the queue is empty.
 #pragma once
 
 #include <algorithm>
@@ -51,16 +54,8 @@ struct ForceArgs {
   int center_limit;    // only user atoms below this act as centers (ghosts above)
   int npad;
   Box box;
-  const int* nbr;      // short list (unfused) or output short list (fused)
+  const int* nbr;      // short list, ELL column-major
   const int* cnt;
-  const int* skin;     // fused filter: skin list input
-  const int* skin_cnt;
-  int* short_out;      // fused filter: short list written as a by-product
-  int* short_cnt_out;
-  double rc, rc2;      // r_cut_max (^2) of the filter (neighbor.cpp:143-152)
-  const float4* posf;  // float shadow for the pre-test
-  const int* cmax;     // |coordinate| bound for the pre-test band
-  BoxF boxf;
   const void* rows;
   const double* cutsq;
   int ns;
@@ -79,7 +74,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // Parameter-table specialisations.
 enum Spec : int {
-  kSingle = 0,   // one species: the row lives in registers
+  kSingle = 0,   // one species: the row comes from the constant bank
   kHoist = 1,    // several species, ramp (R, D) depends on (i, k) only
   kGeneric = 2,  // anything else: ramp and cutoff test per triplet
 };
@@ -129,18 +124,21 @@ template <> struct Stage<float> {
 
 // One (i, j, k) triplet: zeta term and its j and k gradients
 // (potential.hpp:132-198; the i gradient is never formed: F_i = -sum P).
+// A triplet that does not count enters with fck = dfck = 0 and ok = false:
+// every output is then exactly zero (the exponent argument is zeroed too, so
+// no inf can meet the zero), which replaces seven selects per triplet.
 template <typename R>
 __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R fck, R dfck,
-                                           const Row<R>& p) {
+                                           bool ok, const Row<R>& p) {
   Grad<R> o;
   R cs = j.ux * k.ux + j.uy * k.uy + j.uz * k.uz;
   cs = fmin(R(1), fmax(R(-1), cs));
   const R t = p.h - cs;
   const R den = p.d2 + t * t;
-  const R iden = R(1) / den;
+  const R iden = Fn<R>::rcp(den);
   const R g = p.gamma + p.gcd2 * (t * t) * iden;
   const R dg = R(-2) * p.gc2 * t * iden * iden;
-  const R arg = p.lam3 * (j.r - k.r);
+  const R arg = ok ? p.lam3 * (j.r - k.r) : R(0);
   const bool cubic = p.m3 != R(0);
   const R ex = Fn<R>::exp_(cubic ? arg * arg * arg : arg);
   const R dex = ex * p.lam3 * (cubic ? R(3) * arg * arg : R(1));
@@ -164,20 +162,21 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
   return o;
 }
 
-template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FUSED>
+// Loads one tile needs before it can compute: count + list entry (stage A),
+// then the two positions (stage B, dependent on stage A).
+struct TileIdx {
+  int i, n, j;
+};
+
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF>
 __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceArgs<R> a) {
   constexpr bool kCache = G <= 8;     // register cache of d zeta / d x_k
   constexpr int kUnroll = kCache ? G : 2;
   constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
-  constexpr unsigned kGroupMask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
   __shared__ double scut[SPEC == kSingle ? 1 : kRows];
   __shared__ Stage<R> st;
   __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
-  // fused filter: compacted short-list records, slot-indexed
-  __shared__ int s_j[FUSED ? kBlock : 1];
-  __shared__ double2 s_d01[FUSED ? kBlock : 1];   // dx, dy
-  __shared__ double2 s_d2r[FUSED ? kBlock : 1];   // dz, r^2
   __shared__ double s_red[kBlock / 32][kRedWidth];
 
   const int tid = threadIdx.x;
@@ -210,19 +209,56 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
   constexpr int kAtomsPerBlock = kBlock / G;
   const int ntiles = (a.n_owned + kAtomsPerBlock - 1) / kAtomsPerBlock;
   const int nwarps_total = gridDim.x * (kBlock / 32);
+  const int last = a.n_owned - 1;
+
+  // stage A loads: count and this lane's list entry (clamped into range; the
+  // entry past the count is unused, it only keeps the dependent load legal)
+  auto load_idx = [&](int tile) {
+    TileIdx t;
+    t.i = tile * kAtomsPerBlock + tid / G;
+    const bool in = tile < ntiles && t.i < a.n_owned;
+    if (!in) t.i = 0;
+    t.n = in ? a.cnt[t.i] : 0;
+    const int v = in ? a.nbr[std::size_t(gl) * a.npad + t.i] : 0;
+    t.j = unsigned(v) <= unsigned(last) ? v : 0;
+    return t;
+  };
+
   int work = OVF ? blockIdx.x * (kBlock / 32) + tid / 32 : blockIdx.x;
+  TileIdx nxt{0, 0, 0}, nxt2{0, 0, 0};
+  double4 pi_n = make_double4(0, 0, 0, 0), pj_n = pi_n;
+  if (!OVF) {
+    nxt = load_idx(work);
+    pi_n = a.pos[nxt.i];
+    pj_n = a.pos[nxt.j];
+    nxt2 = load_idx(work + gridDim.x);
+  }
 
   while (true) {
-    int i;
+    int i, n_i, j;
+    double4 pi, pj;
     bool active;
     if (OVF) {
       if (work >= n_ovf) break;        // warp-uniform
       i = a.overflow[work];
       active = true;
+      n_i = a.cnt[i];
+      j = gl < n_i ? a.nbr[std::size_t(gl) * a.npad + i] : i;
+      pi = a.pos[i];
+      pj = a.pos[j];
     } else {
       if (work >= ntiles) break;       // block-uniform
-      i = work * kAtomsPerBlock + tid / G;
-      active = i < a.n_owned;
+      i = nxt.i;
+      n_i = nxt.n;
+      j = nxt.j;
+      pi = pi_n;
+      pj = pj_n;
+      // keep the pipeline full: positions of the next tile, list of the one after
+      nxt = nxt2;
+      pi_n = a.pos[nxt.i];
+      pj_n = a.pos[nxt.j];
+      nxt2 = load_idx(work + 2 * gridDim.x);
+      active = work * kAtomsPerBlock + tid / G < a.n_owned;
       // ghost copies (decomposition) receive forces but are not centers
       if (active && (a.perm ? a.perm[i] : i) >= a.center_limit) {
         if (DET && gl == 0) {
@@ -231,57 +267,7 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
         }
         active = false;
       }
-    }
-
-    const double4 pi = a.pos[active ? i : 0];
-    int n_i = 0;
-    if constexpr (FUSED) {
-      // The paper's cutoff filter (Sec. 4.4; neighbor.cpp:143-152) in-kernel:
-      // the group tests G skin entries per round with the reference's exact
-      // FP64 distance, and ballot + popc compacts the survivors into slots.
-      const int m = active ? a.skin_cnt[i] : 0;
-      const int mmax = __reduce_max_sync(kFull, m);
-      float lo, hi;
-      band_for(a.rc, a.cmax, lo, hi);
-      const float4 pfi = a.posf[active ? i : 0];
-      constexpr int kDepth = 4;          // rounds whose loads are in flight together
-      for (int c0 = 0; c0 < mmax; c0 += kDepth * G) {
-        int bb[kDepth];
-        float4 pb[kDepth];
-#pragma unroll
-        for (int u = 0; u < kDepth; ++u) {
-          const int s = c0 + u * G + gl;
-          bb[u] = s < m ? a.skin[std::size_t(s) * a.npad + i] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < kDepth; ++u) pb[u] = a.posf[bb[u] >= 0 ? bb[u] : 0];
-#pragma unroll
-        for (int u = 0; u < kDepth; ++u) {
-          double ex_ = 0, ey_ = 0, ez_ = 0, er2 = 0;
-          bool pass = false;
-          if (bb[u] >= 0 && prefilter(pfi, pb[u], a.boxf, lo, hi) != kOut) {
-            // survivors (and the rare band cases) get the exact FP64 distance
-            displacement(pi, a.pos[bb[u]], a.box, ex_, ey_, ez_);
-            er2 = norm_sq_exact(ex_, ey_, ez_);
-            pass = er2 <= a.rc2;
-          }
-          const unsigned gm = (__ballot_sync(kFull, pass) >> wbase) & kGroupMask;
-          const int q = n_i + __popc(gm & ((1u << gl) - 1u));
-          if (pass) {
-            if (q < G) {
-              s_j[gbase + q] = bb[u];
-              s_d01[gbase + q] = make_double2(ex_, ey_);
-              s_d2r[gbase + q] = make_double2(ez_, er2);
-            }
-            a.short_out[std::size_t(q) * a.npad + i] = bb[u];
-          }
-          n_i += __popc(gm);
-        }
-      }
-      if (active && gl == 0) a.short_cnt_out[i] = n_i;
-      __syncwarp();
-    } else {
-      n_i = active ? a.cnt[i] : 0;
+      if (!active) n_i = 0;
     }
     if (n_i > G) {
       if (gl == 0) {
@@ -292,33 +278,20 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
       active = false;
     }
     const bool slot = gl < n_i;
-    int j;
     double dx = 0, dy = 0, dz = 0, r2 = 1.0;
-    if constexpr (FUSED) {
-      j = slot ? s_j[tid] : (active ? i : 0);
-      if (slot) {
-        const double2 d01 = s_d01[tid], d2r = s_d2r[tid];
-        dx = d01.x;
-        dy = d01.y;
-        dz = d2r.x;
-        r2 = d2r.y;
-      }
-    } else {
-      j = slot ? a.nbr[std::size_t(gl) * a.npad + i] : (active ? i : 0);
-      if (slot) {
-        displacement(pi, a.pos[j], a.box, dx, dy, dz);
-        r2 = norm_sq_exact(dx, dy, dz);
-      }
+    if (slot) {
+      displacement(pi, pj, a.box, dx, dy, dz);
+      r2 = norm_sq_exact(dx, dy, dz);
     }
     const int si = SPEC == kSingle ? 0 : species_of(pi);
-    const int sj = SPEC == kSingle ? 0 : species_of(a.pos[j]);
+    const int sj = SPEC == kSingle ? 0 : species_of(pj);
     const int row_jj = (si * ns + sj) * ns + sj;
     const bool pair_ok = slot && r2 <= (SPEC == kSingle ? cut0 : scut[row_jj]);
     const Row<R>& pjj = SPEC == kSingle ? row0 : srow[row_jj];
 
     Nbr<R> me;
-    me.r = Fn<R>::sqrt_(R(r2));
-    me.ir = R(1) / me.r;
+    me.ir = Fn<R>::rsqrt_(R(r2));      // one rsqrt gives 1/r and r
+    me.r = R(r2) * me.ir;
     me.ux = R(dx) * me.ir;
     me.uy = R(dy) * me.ir;
     me.uz = R(dz) * me.ir;
@@ -355,15 +328,17 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
           cutoff_ramp(k.r, *prow, fck, dfck);
         }
       }
-      const Grad<R> tr = triplet<R>(me, k, fck, dfck, *prow);
-      zeta += ok ? tr.z : R(0);
-      gjx += ok ? tr.jx : R(0);
-      gjy += ok ? tr.jy : R(0);
-      gjz += ok ? tr.jz : R(0);
+      fck = ok ? fck : R(0);
+      dfck = ok ? dfck : R(0);
+      const Grad<R> tr = triplet<R>(me, k, fck, dfck, ok, *prow);
+      zeta += tr.z;
+      gjx += tr.jx;
+      gjy += tr.jy;
+      gjz += tr.jz;
       if constexpr (kCache) {
-        ckx[t] = ok ? tr.kx : R(0);
-        cky[t] = ok ? tr.ky : R(0);
-        ckz[t] = ok ? tr.kz : R(0);
+        ckx[t] = tr.kx;
+        cky[t] = tr.ky;
+        ckz[t] = tr.kz;
       }
     }
 
@@ -387,6 +362,8 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     R pz = -(me.uz * dvdr) - gjz * dvdz;
 
     // ---- scatter pass: lane (l + t) mod n receives lane l's k-gradient ----
+    // Every lane of a group shares n_i, and a sender's gradient for rotation t
+    // is zero unless t < n_i and its triplet counts, so receivers need no mask.
 #pragma unroll kUnroll
     for (int t = 1; t < G; ++t) {
       R sx, sy, sz;
@@ -411,21 +388,19 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
             cutoff_ramp(k.r, *prow, fck, dfck);
           }
         }
-        const Grad<R> tr = triplet<R>(me, k, fck, dfck, *prow);
-        sx = ok ? tr.kx * dvdz : R(0);
-        sy = ok ? tr.ky * dvdz : R(0);
-        sz = ok ? tr.kz * dvdz : R(0);
+        fck = ok ? fck : R(0);
+        dfck = ok ? dfck : R(0);
+        const Grad<R> tr = triplet<R>(me, k, fck, dfck, ok, *prow);
+        sx = tr.kx * dvdz;
+        sy = tr.ky * dvdz;
+        sz = tr.kz * dvdz;
       }
       int s = gl - t;
       if (s < 0) s += n_i;
       const int from = wbase + (s & (G - 1));
-      const R rx = __shfl_sync(kFull, sx, from);
-      const R ry = __shfl_sync(kFull, sy, from);
-      const R rz = __shfl_sync(kFull, sz, from);
-      const bool take = slot && t < n_i;
-      px -= take ? rx : R(0);
-      py -= take ? ry : R(0);
-      pz -= take ? rz : R(0);
+      px -= __shfl_sync(kFull, sx, from);
+      py -= __shfl_sync(kFull, sy, from);
+      pz -= __shfl_sync(kFull, sz, from);
     }
     if (!slot) px = py = pz = 0;
 
@@ -607,10 +582,10 @@ int persistent_blocks(K kernel, int tiles) {
 
 constexpr int kOverflowBlocks = 148;
 
-template <typename R, typename Acc, int G, int SPEC, bool DET, bool FUSED>
+template <typename R, typename Acc, int G, int SPEC, bool DET>
 int launch_main(Ctx& c, ForceArgs<R> a) {
   const int tiles = std::max(1, ceil_div(a.n_owned, kBlock / G));
-  auto kern = k_force<R, Acc, G, SPEC, DET, false, FUSED>;
+  auto kern = k_force<R, Acc, G, SPEC, DET, false>;
   const int blocks = persistent_blocks(kern, tiles);
   a.partial_base = 0;
   c.mark(2);
@@ -620,7 +595,7 @@ int launch_main(Ctx& c, ForceArgs<R> a) {
   return blocks;
 }
 
-template <typename R, typename Acc, int SPEC, bool DET, bool FUSED>
+template <typename R, typename Acc, int SPEC, bool DET>
 void run_force(Ctx& c, ForceArgs<R> a) {
   // Group width from the largest short count seen at the last list build;
   // atoms that outgrow it between rebuilds take the overflow launch.
@@ -628,28 +603,22 @@ void run_force(Ctx& c, ForceArgs<R> a) {
   const int g = mx <= 4 ? 4 : mx <= 8 ? 8 : mx <= 16 ? 16 : 32;
   int nb = 0;
   switch (g) {
-    case 4: nb = launch_main<R, Acc, 4, SPEC, DET, FUSED>(c, a); break;
-    case 8: nb = launch_main<R, Acc, 8, SPEC, DET, FUSED>(c, a); break;
-    case 16: nb = launch_main<R, Acc, 16, SPEC, DET, FUSED>(c, a); break;
-    default: nb = launch_main<R, Acc, 32, SPEC, DET, FUSED>(c, a); break;
+    case 4: nb = launch_main<R, Acc, 4, SPEC, DET>(c, a); break;
+    case 8: nb = launch_main<R, Acc, 8, SPEC, DET>(c, a); break;
+    case 16: nb = launch_main<R, Acc, 16, SPEC, DET>(c, a); break;
+    default: nb = launch_main<R, Acc, 32, SPEC, DET>(c, a); break;
   }
   a.partial_base = nb;
-  k_force<R, Acc, 32, SPEC, DET, true, FUSED><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
+  k_force<R, Acc, 32, SPEC, DET, true><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
   k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb + kOverflowBlocks, c.result.get());
   c.launches += 2;
 }
 
-template <typename R, typename Acc, bool DET, bool FUSED>
-void dispatch_spec(Ctx& c, const ForceArgs<R>& a) {
-  if (c.params.species_count() == 1) run_force<R, Acc, kSingle, DET, FUSED>(c, a);
-  else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET, FUSED>(c, a);
-  else run_force<R, Acc, kGeneric, DET, FUSED>(c, a);
-}
-
 template <typename R, typename Acc, bool DET>
-void dispatch_fused(Ctx& c, const ForceArgs<R>& a, bool fused) {
-  if (fused) dispatch_spec<R, Acc, DET, true>(c, a);
-  else dispatch_spec<R, Acc, DET, false>(c, a);
+void dispatch_spec(Ctx& c, const ForceArgs<R>& a) {
+  if (c.params.species_count() == 1) run_force<R, Acc, kSingle, DET>(c, a);
+  else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET>(c, a);
+  else run_force<R, Acc, kGeneric, DET>(c, a);
 }
 
 template <typename R, typename Acc>
@@ -668,19 +637,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.center_limit = int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
   a.npad = npad;
   a.box = c.box;
-  // fused: the kernel filters the skin list itself and writes the short list
-  const bool fused = (flags & 0x2u) == 0 && c.fuse_filter;
   a.nbr = c.short_list.nbr.get();
   a.cnt = c.short_list.cnt.get();
-  a.skin = c.skin_list.nbr.get();
-  a.skin_cnt = c.skin_list.cnt.get();
-  a.short_out = c.short_list.nbr.get();
-  a.short_cnt_out = c.short_list.cnt.get();
-  a.rc = c.params.r_cut_max();
-  a.rc2 = c.params.r_cut_max() * c.params.r_cut_max();
-  a.posf = c.posf.get();
-  a.cmax = c.flags.get() + 5;
-  a.boxf = c.boxf;
   a.rows = std::is_same<R, double>::value ? static_cast<const void*>(c.rows_f64.get())
                                           : static_cast<const void*>(c.rows_f32.get());
   a.cutsq = c.cutsq.get();
@@ -703,7 +661,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     a.slot_y = c.py.get();
     a.slot_z = c.pz.get();
     a.fself = c.fself.get();
-    dispatch_fused<R, Acc, true>(c, a, fused);
+    dispatch_spec<R, Acc, true>(c, a);
     if (n > 0) {
       k_gather<Acc><<<ceil_div(n, kBlock), kBlock, 0, c.stream>>>(
           int(n), npad, a.nbr, a.cnt, static_cast<const Acc*>(a.slot_x),
@@ -721,7 +679,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     }
     TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
     a.forces = target;
-    dispatch_fused<R, Acc, false>(c, a, fused);
+    dispatch_spec<R, Acc, false>(c, a);
     if (kF32 && n > 0) {
       k_to_double<<<ceil_div(3 * n, 256), 256, 0, c.stream>>>(
           reinterpret_cast<const float*>(target), c.forces.get(), 3 * n);
