@@ -520,7 +520,7 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
         if (b < 0 || b >= c.n || b == a)
           throw tsf::ConfigError("neighbor index out of range in segment of atom " +
                                  std::to_string(a));
-        ell[std::size_t(s - offsets[a]) * c.npad + a] = b;
+        ell[tsf::ell_at(s - offsets[a], int(a), c.npad)] = b;
       }
     }
     c.skin_list.cap = cap;
@@ -578,7 +578,7 @@ int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbr
       const int a = slot_of[std::size_t(u)];
       const int m = cnt[std::size_t(a)];
       if (w + m > cap) throw tsf::ConfigError("neighbor export buffer too small");
-      for (int q = 0; q < m; ++q) nbrs[w + q] = perm[std::size_t(ell[std::size_t(q) * c.npad + a])];
+      for (int q = 0; q < m; ++q) nbrs[w + q] = perm[std::size_t(ell[tsf::ell_at(q, a, c.npad)])];
       std::sort(nbrs + w, nbrs + w + m);
       w += m;
       offsets[u + 1] = int32_t(w);

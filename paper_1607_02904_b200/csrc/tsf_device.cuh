@@ -59,6 +59,14 @@ __device__ __forceinline__ void displacement(const double4& a, const double4& b,
 
 __device__ __forceinline__ int species_of(const double4& p) { return int(p.w); }
 
+// Neighbor lists: "ELL4" — column-major ELL in blocks of 4 slots, so a thread
+// fetches 4 entries of its atom with one 128-bit load (coalesced across the
+// consecutive atoms of a warp) and a 4-lane group reads 16 contiguous bytes.
+// Capacities are multiples of 4.
+__host__ __device__ __forceinline__ std::size_t ell_at(int s, int a, int npad) {
+  return (std::size_t(s >> 2) * std::size_t(npad) + std::size_t(a)) * 4 + std::size_t(s & 3);
+}
+
 // Float shadow of the positions (slot order, {x, y, z, species}) for cheap
 // pre-tests.  A pre-test decides "inside" / "outside" only when the float
 // squared distance clears the cutoff by more than its worst-case error

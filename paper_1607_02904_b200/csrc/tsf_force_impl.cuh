@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     const bool in = tile < ntiles && t.i < a.n_owned;
     if (!in) t.i = 0;
     t.n = in ? a.cnt[t.i] : 0;
-    const int v = in ? a.nbr[std::size_t(gl) * a.npad + t.i] : 0;
+    const int v = in ? a.nbr[ell_at(gl, t.i, a.npad)] : 0;
     t.j = unsigned(v) <= unsigned(last) ? v : 0;
     return t;
   };
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
       i = a.overflow[work];
       active = true;
       n_i = a.cnt[i];
-      j = gl < n_i ? a.nbr[std::size_t(gl) * a.npad + i] : i;
+      j = gl < n_i ? a.nbr[ell_at(gl, i, a.npad)] : i;
       pi = a.pos[i];
       pj = a.pos[j];
     } else {
@@ -504,10 +504,10 @@ __global__ void __launch_bounds__(kBlock) k_gather(int n, int npad, const int* _
       fz = fself[3 * std::size_t(a) + 2];
   const int m = cnt[a];
   for (int s = 0; s < m; ++s) {
-    const int b = nbr[std::size_t(s) * npad + a];
+    const int b = nbr[ell_at(s, a, npad)];
     const int mb = cnt[b];
     for (int t = 0; t < mb; ++t) {
-      if (nbr[std::size_t(t) * npad + b] == a) {
+      if (nbr[ell_at(t, b, npad)] == a) {
         const std::size_t q = std::size_t(t) * npad + b;
         fx += sx[q];
         fy += sy[q];

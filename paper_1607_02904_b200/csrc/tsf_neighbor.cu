@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
     }
     buf[j + 1] = v;
   }
-  for (int s = 0; s < m; ++s) nbr[std::size_t(s) * a.npad + at] = buf[s];
+  for (int s = 0; s < m; ++s) nbr[ell_at(s, at, a.npad)] = buf[s];
   cnt[at] = m;
 }
 
@@ -185,13 +185,14 @@ __global__ void __launch_bounds__(kBlock) k_filter(
     float lo, hi;
     band_for(rc, a.cmax, lo, hi);
     const float4 pfa = a.posf[at];
-    constexpr int kDepth = 4;   // loads in flight per thread
+    constexpr int kDepth = 4;   // one 128-bit list load per 4 candidates (ELL4)
     for (int s0 = 0; s0 < m; s0 += kDepth) {
-      int bb[kDepth];
+      // the list is streamed once per step: evict-first keeps the gathered
+      // position shadow resident in L2
+      const int4 q = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(s0, at, a.npad)));
+      int bb[kDepth] = {q.x, s0 + 1 < m ? q.y : -1, s0 + 2 < m ? q.z : -1,
+                        s0 + 3 < m ? q.w : -1};
       float4 pb[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u)
-        bb[u] = s0 + u < m ? skin[std::size_t(s0 + u) * a.npad + at] : -1;
 #pragma unroll
       for (int u = 0; u < kDepth; ++u) pb[u] = a.posf[bb[u] >= 0 ? bb[u] : at];
 #pragma unroll
@@ -203,12 +204,11 @@ __global__ void __launch_bounds__(kBlock) k_filter(
           displacement(a.pos[at], a.pos[bb[u]], a.box, dx, dy, dz);
           v = norm_sq_exact(dx, dy, dz) <= rc2 ? kIn : kOut;
         }
-        if (v == kIn) out[std::size_t(w++) * a.npad + at] = bb[u];
+        if (v == kIn) out[ell_at(w++, at, a.npad)] = bb[u];
       }
     }
   } else {
-    for (int s = 0; s < m; ++s)
-      out[std::size_t(s) * a.npad + at] = skin[std::size_t(s) * a.npad + at];
+    for (int s = 0; s < m; ++s) out[ell_at(s, at, a.npad)] = skin[ell_at(s, at, a.npad)];
     w = m;
   }
   out_cnt[at] = w;
