@@ -235,6 +235,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -368,7 +369,8 @@ def main():
         lib = L.lib()
         hx = torch.from_numpy(xyz.copy()).pin_memory()
         hf = torch.empty((n, 3), dtype=torch.float64).pin_memory()
-        sp = np.ascontiguousarray(species, np.int32)
+        sp_t = torch.from_numpy(np.ascontiguousarray(species, np.int32)).pin_memory()
+        sp = sp_t.numpy()               # page-locked: species go straight to the device
         bx = np.ascontiguousarray(box, np.float64)
         pr = np.ascontiguousarray(per, np.uint8)
         energy = C.c_double()
@@ -404,6 +406,33 @@ def main():
                "d2h_bytes_per_step": int(hf.numel() * 8 + 8 + 48),
                "ms_per_step": 1e3 * te / args.steps,
                "call": "tsf_evaluate_forces (include/tersoff_b200.h), pinned host buffers"}
+
+    # the other precisions on the same resident system (device-resident only)
+    variants = {}
+    if world == 1 and not args.no_variants:
+        for prec in [p for p in DTYPES if p != args.precision]:
+            def vstep(prec=prec):
+                ctx.compute(prec, deterministic=args.deterministic, energy=False, forces=False,
+                            virial=False)
+            for _ in range(args.warmup):
+                vstep()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                vstep()
+            e1.record(stream)
+            e1.synchronize()
+            tv = e0.elapsed_time(e1) / 1e3
+            ctx.profile(True)
+            for _ in range(args.steps):
+                vstep()
+            pv = ctx.profile_read(reset=True)
+            ctx.profile(False)
+            kms = pv["force_ms"] / max(pv["calls"], 1)
+            vpeak, _ = load_peak(prec)
+            variants[prec] = {"value": n * args.steps / tv, "ms_per_step": 1e3 * tv / args.steps,
+                              "dtype": DTYPES[prec], "kernel_ms": kms,
+                              "roofline_frac": algo_flop / (kms * 1e-3) / 1e12 / vpeak}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -442,6 +471,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "variants": variants,
             "gpu_launches": launches,
             "clocks": clk,
         }

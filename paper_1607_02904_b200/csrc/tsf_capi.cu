@@ -144,7 +144,10 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
   if (n < 0 || n > (std::int64_t(1) << 30)) throw tsf::ConfigError("atom count out of range");
   for (int ax = 0; ax < 3; ++ax)
     if (!(box[ax] > 0.0)) throw tsf::ConfigError("simulation box edges must be positive");
-  check_species(c, n, species);
+  // page-locked species go straight to the device and are validated there (no
+  // O(n) host pass per call); pageable ones are checked and cached on the host
+  const bool sp_pinned = n > 0 && is_pinned(species);
+  if (!sp_pinned) check_species(c, n, species);
   bool geometry_changed = n != c.n;
   for (int ax = 0; ax < 3; ++ax) {
     geometry_changed |= c.box.len[ax] != box[ax] || c.box.per[ax] != int(per[ax] != 0);
@@ -173,9 +176,14 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.short_list.valid = false;
     c.tiled = false;
   }
-  // species change rarely: re-upload only when they differ from the last upload
-  if (n > 0 && (c.host_species.size() != std::size_t(n) ||
-                std::memcmp(c.host_species.data(), species, sizeof(int) * n) != 0)) {
+  if (sp_pinned) {
+    TSF_CUDA(cudaMemcpyAsync(c.species.get(), species, sizeof(int) * n, cudaMemcpyHostToDevice,
+                             c.stream));
+    tsf::validate_species(c, c.has_potential ? c.params.species_count() : kMaxListSpecies);
+    c.host_species.clear();
+  } else if (n > 0 && (c.host_species.size() != std::size_t(n) ||
+                       std::memcmp(c.host_species.data(), species, sizeof(int) * n) != 0)) {
+    // species change rarely: re-upload only when they differ from the last upload
     c.host_species.assign(species, species + n);
     TSF_CUDA(cudaMemcpyAsync(c.species.get(), c.host_species.data(), sizeof(int) * n,
                              cudaMemcpyHostToDevice, c.stream));
@@ -202,12 +210,17 @@ void download_forces(Ctx& c, double* forces) {
 }
 
 void raise_device_errors(Ctx& c) {
-  int f = 0;
-  TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  int f[8] = {0};
+  TSF_CUDA(cudaMemcpyAsync(f, c.flags.get(), sizeof f, cudaMemcpyDeviceToHost, c.stream));
   TSF_CUDA(cudaStreamSynchronize(c.stream));
-  if (f & tsf::kErrShortOverflow)
+  if (f[7] & tsf::kErrBadSpecies) {
+    TSF_CUDA(cudaMemsetAsync(c.flags.get() + 7, 0, sizeof(int), c.stream));
+    c.host_species.clear();
+    throw tsf::ConfigError("a species id lies outside the parameter table's species");
+  }
+  if (f[0] & tsf::kErrShortOverflow)
     throw tsf::ConfigError("an atom has more than 32 neighbours within r_cut_max");
-  if (f & tsf::kErrNonFinite) throw tsf::NumericError("non-finite pair term");
+  if (f[0] & tsf::kErrNonFinite) throw tsf::NumericError("non-finite pair term");
 }
 
 void finish(Ctx& c, double* energy, double* forces, double* virial) {

@@ -139,6 +139,9 @@ void upload_params(Ctx& c);
 // error bits in flags[0]
 constexpr int kErrShortOverflow = 1;   // an atom has more than 32 short neighbours
 constexpr int kErrNonFinite = 2;       // non-finite pair term
+constexpr int kErrBadSpecies = 4;      // species id out of range (device-side check)
+
+void validate_species(Ctx& c, int nspecies);   // sets kErrBadSpecies in flags[0]
 
 void pack_positions(Ctx& c);           // xyz_stage + species (user order) -> pos (slots)
 void unpack_positions(Ctx& c);         // pos (slots) -> xyz_stage (user order)

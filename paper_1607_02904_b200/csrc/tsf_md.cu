@@ -203,6 +203,23 @@ const int* inv_of(const Ctx& c) { return c.sorted ? c.inv.get() : nullptr; }
 
 }  // namespace
 
+namespace {
+__global__ void k_check_species(const int* __restrict__ species, int n, int ns,
+                                int* __restrict__ flags) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool bad = a < n && (species[a] < 0 || species[a] >= ns);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, kErrBadSpecies);
+}
+}  // namespace
+
+void validate_species(Ctx& c, int nspecies) {
+  if (c.n == 0) return;
+  // flags[7]: survives the per-evaluation reset of flags[0..1]
+  k_check_species<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.species.get(), int(c.n), nspecies,
+                                                            c.flags.get() + 7);
+  ++c.launches;
+}
+
 void gather_positions(Ctx& c, const int* d_idx, std::int64_t m, double* d_xyz) {
   if (m <= 0) return;
   k_gather_pos<<<blocks_for(m), kBlock, 0, c.stream>>>(c.pos.get(), inv_of(c), d_idx, int(m),
