@@ -42,6 +42,10 @@ CONFIGS = {
     "si32k": ((20, 20, 10), 5.431, 0.15, "si", "BASELINE cfg 2 size: Si diamond 20x20x10 = 32,000 atoms"),
     "sic256k": ((32, 32, 32), 4.32, 0.10, "sic",
                 "BASELINE cfg 3: 3C-SiC zincblende 32^3 = 262,144 atoms"),
+    "liquid512k": ((40, 40, 40), 5.431, 0.0, "si",
+                   "BASELINE cfg 5: liquid Si 40^3 cells = 512,000 atoms, melted at 6000 K "
+                   "(2 ps) and held at 3000 K (4 ps), dt 0.5 fs, velocity rescaling every 50 "
+                   "steps (SURVEY.md 8d)"),
 }
 DTYPES = {"double": "f64", "mixed": "f32 compute / f64 accumulate", "single": "f32"}
 REF_OPTS = {"double": ("v1", "opt-d", 4), "mixed": ("v2", "opt-m", 8),
@@ -61,6 +65,9 @@ def make_system(cfg: str):
     s = tb.make_diamond_lattice(*cells, a0)
     rng = np.random.default_rng(12345)
     xyz = np.mod(s.positions + rng.uniform(-jitter, jitter, s.positions.shape), s.box.lengths)
+    if cfg.startswith("liquid"):
+        # input preparation (untimed): the GPU melt protocol of SURVEY.md 8d cfg 5
+        xyz = tb.melt(s, tb.builtin_silicon()).positions
     if pkind == "sic":
         text = open(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")).read()
         species = np.where(np.arange(s.natoms) % 8 < 4, 0, 1).astype(np.int32)

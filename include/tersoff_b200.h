@@ -163,6 +163,9 @@ int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel);
 int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t flags,
                int thermo_every, double* thermo, int64_t cap, int64_t* nsamples,
                int64_t* rebuilds);
+/* v *= factor for every atom (velocity-rescaling thermostat for fixture
+ * generation, e.g. the liquid-Si melt of SURVEY.md 8d cfg 5). */
+int tsf_md_scale_velocities(tsf_ctx* ctx, double factor);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     kinetic_energy,
     load_params,
     make_diamond_lattice,
+    melt,
     needs_rebuild,
     parse_params,
     perturbed_lattice,

@@ -385,6 +385,9 @@ class Context:
         m = np.ascontiguousarray(masses, dtype=np.float64)
         self._ok(self._lib.tsf_md_set_state(self._h, _ptr(v), _ptr(m)))
 
+    def md_scale_velocities(self, factor: float):
+        self._ok(self._lib.tsf_md_scale_velocities(self._h, float(factor)))
+
     def md_get_state(self):
         x = np.zeros((self.n, 3))
         v = np.zeros((self.n, 3))
@@ -555,3 +558,33 @@ def run_nve(system: AtomSystem, params: ParamTable, steps: int, dt: float = 0.00
             "scheme": "gpu-group", "precision": PRECISION_NAMES[p],
             "width": width or (4 if p == 0 else 8), "neighbor_rebuilds": rebuilds,
             "csv": "\n".join(rows) + "\n", "system": final}
+
+
+def melt(system: AtomSystem, params: ParamTable, hot_temperature: float = 6000.0,
+         hot_ps: float = 2.0, temperature: float = 3000.0, hold_ps: float = 4.0,
+         dt: float = 0.0005, rescale_every: int = 50, seed: int = 12345,
+         precision: str = "double") -> AtomSystem:
+    """Liquid fixture generator (SURVEY.md 8d cfg 5): Maxwell-Boltzmann at
+    `hot_temperature`, hold there for `hot_ps`, then at `temperature` for
+    `hold_ps`, velocity-Verlet with velocity rescaling every `rescale_every`
+    steps — GPU-resident (tsf_md_run + tsf_md_scale_velocities)."""
+    work = system.copy()
+    init_velocities(work, hot_temperature, seed)
+    ctx = Context(params)
+    ctx.load(work)
+    ctx.build_neighbor_list(params.r_cut_max, 1.0)
+    ctx.md_set_state(work.velocities, work.species_masses)
+    n = work.natoms
+    for target, ps in ((hot_temperature, hot_ps), (temperature, hold_ps)):
+        blocks = max(1, int(round(ps / dt / rescale_every)))
+        for _ in range(blocks):
+            thermo, _ = ctx.md_run(rescale_every, dt, precision, False, rescale_every)
+            t_now = 2.0 * thermo[-1, 2] / (3.0 * n * K_BOLTZMANN)
+            if t_now > 0:
+                ctx.md_scale_velocities(np.sqrt(target / t_now))
+    x, v = ctx.md_get_state()
+    ctx.close()
+    out = work.copy()
+    out.positions, out.velocities = x, v
+    out.forces = np.zeros_like(x)
+    return out

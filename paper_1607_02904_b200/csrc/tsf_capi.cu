@@ -380,9 +380,9 @@ int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
     c.device = device;
     TSF_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = c.stream;
-    c.flags.reserve(8);
+    c.flags.reserve(16);
     c.result.reserve(8);
-    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 8 * sizeof(int), c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 16 * sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.result.get(), 0, 8 * sizeof(double), c.stream));
     tsf::upload_params(c);
     c.masses.assign(std::size_t(c.params.species_count()), 28.0855);
@@ -658,6 +658,13 @@ int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel) {
                              cudaMemcpyDeviceToHost, c.stream));
     TSF_CUDA(cudaStreamSynchronize(c.stream));
     std::memcpy(vel, c.pinned, m * sizeof(double));
+  });
+}
+
+int tsf_md_scale_velocities(tsf_ctx* ctx, double factor) {
+  return guard(&ctx->c, [&] {
+    if (!(factor >= 0.0)) throw tsf::ConfigError("velocity scale must be non-negative");
+    tsf::md_scale_velocities(ctx->c, factor);
   });
 }
 

@@ -40,6 +40,7 @@ struct ListState {
   DevBuf<int> nbr;             // [cap * npad]
   DevBuf<int> cnt;             // [npad]
   int max_count = 0;           // host copy, from the last build / filter
+  int over4 = 0, over8 = 0;    // atoms with more than 4 / 8 entries (short list)
   bool valid = false;
 };
 
@@ -102,7 +103,9 @@ struct Ctx {
   DevBuf<double> partials;     // [blocks][kRedWidth]
   DevBuf<double> result;       // energy + virial (7), reduced
   DevBuf<int> flags;           // [0] error bits, [1] overflow count, [2] rebuild flag,
-                               // [3] largest skin count, [4] largest short count
+                               // [3] largest skin count, [4] largest short count,
+                               // [5] |coord| max bits, [6] max cell occupancy,
+                               // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
   DevBuf<int> overflow;        // atoms with more short neighbors than the group width
 
   // MD state
@@ -157,6 +160,7 @@ void pack_velocities(Ctx& c);          // xyz_stage (user order velocities) -> v
 void unpack_velocities(Ctx& c);        // vel (slots) -> xyz_stage (user order)
 void md_kick(Ctx& c, double dt, bool drift);   // v += F dt/(2 m mvv2e) [; x += v dt, wrap]
 void md_kinetic(Ctx& c);               // KE -> result[7] (device)
+void md_scale_velocities(Ctx& c, double factor);
 
 void ensure_pinned(Ctx& c, std::size_t doubles);
 

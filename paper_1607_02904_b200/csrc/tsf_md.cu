@@ -212,6 +212,20 @@ __global__ void k_check_species(const int* __restrict__ species, int n, int ns,
 }
 }  // namespace
 
+namespace {
+__global__ void k_scale(double* __restrict__ v, std::size_t m, double f) {
+  const std::size_t q = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < m) v[q] *= f;
+}
+}  // namespace
+
+void md_scale_velocities(Ctx& c, double factor) {
+  if (c.n == 0) return;
+  k_scale<<<blocks_for(3 * c.n), kBlock, 0, c.stream>>>(c.vel.get(), 3 * std::size_t(c.n),
+                                                        factor);
+  ++c.launches;
+}
+
 void validate_species(Ctx& c, int nspecies) {
   if (c.n == 0) return;
   // flags[7]: survives the per-evaluation reset of flags[0..1]

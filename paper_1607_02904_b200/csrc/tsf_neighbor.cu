@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
 __global__ void __launch_bounds__(kBlock) k_filter(
     ListArgs a, double rc, double rc2, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
-    int* __restrict__ max_count) {
+    int* __restrict__ max_count, int* __restrict__ hist) {
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
   const int m = skin_cnt[at];
@@ -213,6 +213,16 @@ __global__ void __launch_bounds__(kBlock) k_filter(
   }
   out_cnt[at] = w;
   warp_atomic_max(max_count, w);
+  // occupancy histogram for the force kernel's group width (after rebuilds
+  // only): hist[0] = atoms with more than 4 short neighbours, hist[1] = more than 8
+  if (hist) {
+    const unsigned act = __activemask();
+    const int c4 = __popc(__ballot_sync(act, w > 4)), c8 = __popc(__ballot_sync(act, w > 8));
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+      if (c4) atomicAdd(hist, c4);
+      if (c8) atomicAdd(hist + 1, c8);
+    }
+  }
 }
 
 __global__ void k_needs_rebuild(const double4* __restrict__ pos,
@@ -437,23 +447,28 @@ void list_filter(Ctx& c, double r_cut_max, bool apply) {
   s.nbr.reserve(std::size_t(s.cap) * c.npad + 1);
   s.cnt.reserve(std::size_t(c.npad) + 1);
   const bool reread = c.short_max_stale || c.short_apply != int(apply);
-  if (reread) TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
+  if (reread) {
+    TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.flags.get() + 8, 0, 2 * sizeof(int), c.stream));
+  }
   if (c.n > 0) {
     k_filter<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
         list_args(c), r_cut_max, r_cut_max * r_cut_max, apply ? 1 : 0, c.skin_list.nbr.get(),
-        c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), c.flags.get() + 4);
+        c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), c.flags.get() + 4,
+        reread ? c.flags.get() + 8 : nullptr);
     ++c.launches;
   }
   s.valid = true;
   if (reread) {
-    // Largest short count sizes the force kernel's lane group; read it back
-    // only after a rebuild — between rebuilds outgrown atoms take the
+    // The short-count distribution sizes the force kernel's lane group; read
+    // it back only after a rebuild — between rebuilds outgrown atoms take the
     // overflow path, so the steady state never synchronizes here.
-    int mx = 0;
-    TSF_CUDA(cudaMemcpyAsync(&mx, c.flags.get() + 4, sizeof(int), cudaMemcpyDeviceToHost,
-                             c.stream));
+    int f[10] = {0};
+    TSF_CUDA(cudaMemcpyAsync(f, c.flags.get(), sizeof f, cudaMemcpyDeviceToHost, c.stream));
     TSF_CUDA(cudaStreamSynchronize(c.stream));
-    s.max_count = mx;
+    s.max_count = f[4];
+    s.over4 = f[8];
+    s.over8 = f[9];
     c.short_max_stale = false;
     c.short_apply = int(apply);
   }

@@ -261,6 +261,29 @@ def test_evaluate_forces_api(tb, oracle):
         tb.evaluate_forces(s, lst, params, scheme="ref", precision="single")
 
 
+def test_melted_liquid(tb, oracle):
+    """A real liquid (GPU melt, SURVEY.md 8d cfg 5 protocol, shortened):
+    irregular short counts, atoms in the cutoff ramp, G = 8/16 groups."""
+    s = tb.melt(tb.make_diamond_lattice(3, 3, 3), tb.builtin_silicon(), hot_ps=0.25,
+                hold_ps=0.25)
+    case = systems.Case("melt216", s.positions, s.species, s.box.lengths, s.box.periodic, 1.0,
+                        systems.si_text(tb))
+    params, ctx = _ctx(tb, case)
+    op, off, nb, ref = _oracle(oracle, case, params)
+    goff, gnb = ctx.export_neighbors("skin")
+    assert np.array_equal(goff, off) and np.array_equal(gnb, nb)
+    soff, _ = ctx.export_neighbors("short")
+    assert np.diff(soff).max() > 4 and np.diff(soff).min() < 4
+    for det in (True, False):
+        e, f, _ = ctx.compute("double", deterministic=det)
+        assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D
+        for prec in ("mixed", "single"):
+            e, f, _ = ctx.compute(prec, deterministic=det)
+            assert abs(e - ref["energy"]) <= E_TOL_M * abs(ref["energy"])
+            assert np.abs(f - ref["forces"]).max() <= F_TOL_M * np.abs(ref["forces"]).max()
+
+
 def test_large_n_against_compensated_oracle(tb, oracle):
     """32k atoms (cfg-2 size): energy vs the long-double oracle sum."""
     s = tb.make_diamond_lattice(20, 20, 10)
