@@ -12,7 +12,8 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtersoff_b200.so")
+# TSF_LIBRARY: an alternative build of the same sources (side-by-side experiments)
+LIB_PATH = os.environ.get("TSF_LIBRARY") or os.path.join(HERE, "libtersoff_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 TSF_OK, TSF_ERR_INTERNAL, TSF_ERR_CONFIG, TSF_ERR_NUMERIC, TSF_ERR_CUDA = 0, 1, 2, 3, 4

@@ -245,8 +245,10 @@ void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
   // The short list is rebuilt from the skin list on every evaluation, as the
   // reference does (kernels.hpp:187-188).  A filter fused into the force
   // kernel measured slower at 2M atoms (0.90 vs 0.66 ms, f64, profiles/r01):
-  // its gathers then sit in the low-occupancy FP64 kernel.
-  tsf::list_filter(c, c.params.r_cut_max(), (flags & TSF_NO_FILTER) == 0);
+  // its gathers then sit in the low-occupancy FP64 kernel.  Pairs beyond
+  // every cutoff of their species pair are dropped here as well: they add
+  // exact zeros in the reference (the kernel tests the same exact r^2).
+  tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
   c.mark(1);
   tsf::compute(c, p, flags);
   c.mark(4);
@@ -288,7 +290,7 @@ const tsf::ListState& list_for(Ctx& c, int which) {
   if (which == TSF_LIST_SKIN) return c.skin_list;
   if (which != TSF_LIST_SHORT) throw tsf::ConfigError("unknown list selector");
   if (!c.has_potential) throw tsf::ConfigError("the short list needs a parameter table");
-  tsf::list_filter(c, c.params.r_cut_max(), true);
+  tsf::list_filter(c, tsf::FilterMode::Cutoff);
   return c.short_list;
 }
 

@@ -129,7 +129,11 @@ struct Ctx {
 
 // ---- kernels (tsf_neighbor.cu) ----
 void list_build(Ctx& c, double cutoff, double skin);
-void list_filter(Ctx& c, double r_cut_max, bool apply);
+// Short list from the skin list: a verbatim copy (filter off), the
+// reference's r_cut_max test (exports), or the per species-pair bounds the
+// force path uses (PairBounds; identical to Cutoff for one species).
+enum class FilterMode { Copy = 0, Cutoff = 1, Pair = 2 };
+void list_filter(Ctx& c, FilterMode mode);
 bool list_needs_rebuild(Ctx& c);
 void snapshot_reference_positions(Ctx& c);
 

@@ -104,15 +104,29 @@ __device__ __forceinline__ void band_for(double cut, const int* cmax, float& lo,
   hi = __double2float_ru(cut * cut + er2);
 }
 
+// Short-list bound per (species of i, species of k): the largest squared
+// cutoff of any parameter row (i, *, k).  Every pair the force kernel can
+// accept passes it (the kernel tests the same exact FP64 r^2 against
+// cutsq[i][j][k]); the reference's own filter uses r_cut_max for all pairs
+// (kernels.hpp:187-188), which list exports reproduce.
+struct PairBounds {
+  double c2[kMaxSpecies * kMaxSpecies];
+  double cut[kMaxSpecies * kMaxSpecies];
+  int ns;
+};
+
 __device__ __forceinline__ int prefilter(const float4& a, const float4& b, const BoxF& box,
                                          float lo, float hi) {
   float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+  // one conditional +-L per periodic axis, as selects (no branches); the
+  // choice is made on the unwrapped d, exactly as "if d > h: d -= L elif
+  // d < -h: d += L"
 #pragma unroll
-  for (int ax = 0; ax < 3; ++ax)
-    if (box.per[ax]) {
-      if (d[ax] > box.half[ax]) d[ax] -= box.len[ax];
-      else if (d[ax] < -box.half[ax]) d[ax] += box.len[ax];
-    }
+  for (int ax = 0; ax < 3; ++ax) {
+    const float h = box.per[ax] ? box.half[ax] : __int_as_float(0x7f800000);
+    const float dm = d[ax] - box.len[ax], dp = d[ax] + box.len[ax];
+    d[ax] = d[ax] > h ? dm : (d[ax] < -h ? dp : d[ax]);
+  }
   const float r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
   return r2 < lo ? kIn : (r2 > hi ? kOut : kUnsure);
 }

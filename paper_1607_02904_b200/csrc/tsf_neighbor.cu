@@ -11,6 +11,8 @@
 //     to user indices and sorted ascending (neighbor.cpp:114).
 //   filter_all_segments  proj/src/neighbor.cpp:143-180 — skin entries with
 //     r^2 <= r_cut_max^2, order kept; verbatim copy when the filter is off.
+//     (Exports; the force path keeps r^2 <= max_j cutsq[i][j][k] per species
+//     pair, which drops only pairs whose every term is an exact zero.)
 //   needs_rebuild        proj/src/neighbor.cpp:134-141 — any |dx|^2 > (skin/2)^2.
 //
 // Layout and kernels:
@@ -170,52 +172,121 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
   cnt[at] = m;
 }
 
-// Short list, one thread per slot: skin entries with r^2 <= r_cut_max^2 in
-// segment order (float pre-test, exact FP64 inside the band), or a verbatim
-// copy when the filter is off.
-__global__ void __launch_bounds__(kBlock) k_filter(
-    ListArgs a, double rc, double rc2, int apply, const int* __restrict__ skin,
+// Short list, one thread per slot: skin entries that pass their pair's bound,
+// in segment order.  The first 16 entries' ELL4 blocks are all requested
+// before any is tested, so a thread keeps 64 B of list in flight (one block
+// at a time measured latency-bound: 14.7 cycles/issue, 18% of HBM; a quad of
+// lanes per slot was slower still, profiles/r01/ncu).  Float pre-test, exact
+// FP64 inside the band; a verbatim copy when the filter is off.
+#ifndef TSF_FILTER_MINB
+#define TSF_FILTER_MINB 8
+#endif
+
+// Pre-test bands per species pair (shared memory); with one species the
+// single band lives in registers (MULTI = false).
+struct FilterBands {
+  const float* lo;
+  const float* hi;
+  const double* c2;
+  int ns;
+  float lo0, hi0;
+  double c20;
+};
+
+// Bits of the `valid` (1..4) entries of ELL4 block e that are in range.
+template <bool MULTI>
+__device__ __forceinline__ int filter_block(const ListArgs& a, const FilterBands& fb, int at,
+                                            const float4& pfa, int si, int4 e, int valid) {
+  const int bb[4] = {e.x, valid > 1 ? e.y : at, valid > 2 ? e.z : at, valid > 3 ? e.w : at};
+  float4 pf[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) pf[u] = a.posf[bb[u]];
+  int bits = 0, unsure = 0, prs = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (u >= valid) break;
+    int v;
+    if (MULTI) {
+      const int pr = si * fb.ns + min(max(int(pf[u].w), 0), fb.ns - 1);
+      v = prefilter(pfa, pf[u], a.boxf, fb.lo[pr], fb.hi[pr]);
+      prs |= pr << (4 * u);
+    } else {
+      v = prefilter(pfa, pf[u], a.boxf, fb.lo0, fb.hi0);
+    }
+    bits |= (v == kIn) << u;
+    unsure |= (v == kUnsure) << u;
+  }
+  // rare: pairs inside the float error band take the exact FP64 test after
+  // the shadow gathers are dead (keeps the hot path spill-free)
+  while (unsure) {
+    const int u = __ffs(unsure) - 1;
+    unsure &= unsure - 1;
+    const int b = u == 0 ? e.x : u == 1 ? e.y : u == 2 ? e.z : e.w;
+    double dx, dy, dz;
+    displacement(a.pos[at], a.pos[b], a.box, dx, dy, dz);
+    const double c2 = MULTI ? fb.c2[prs >> (4 * u) & 15] : fb.c20;
+    if (norm_sq_exact(dx, dy, dz) <= c2) bits |= 1 << u;
+  }
+  return bits;
+}
+
+__device__ __forceinline__ void keep_block(int* out, int at, int npad, int4 e, int bits, int& w) {
+  if (bits & 1) out[ell_at(w++, at, npad)] = e.x;
+  if (bits & 2) out[ell_at(w++, at, npad)] = e.y;
+  if (bits & 4) out[ell_at(w++, at, npad)] = e.z;
+  if (bits & 8) out[ell_at(w++, at, npad)] = e.w;
+}
+
+template <bool MULTI>
+__global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
+    ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
     int* __restrict__ max_count, int* __restrict__ hist) {
+  __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
+  __shared__ double sc2[kMaxSpecies * kMaxSpecies];
+  const int ns = pb.ns;
+  if (apply && int(threadIdx.x) < ns * ns) {
+    float lo, hi;
+    band_for(pb.cut[threadIdx.x], a.cmax, lo, hi);
+    slo[threadIdx.x] = lo;
+    shi[threadIdx.x] = hi;
+    sc2[threadIdx.x] = pb.c2[threadIdx.x];
+  }
+  __syncthreads();
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
   const int m = skin_cnt[at];
   int w = 0;
   if (apply) {
-    float lo, hi;
-    band_for(rc, a.cmax, lo, hi);
+    const FilterBands fb{slo, shi, sc2, ns, slo[0], shi[0], sc2[0]};
     const float4 pfa = a.posf[at];
-    constexpr int kDepth = 4;   // one 128-bit list load per 4 candidates (ELL4)
-    for (int s0 = 0; s0 < m; s0 += kDepth) {
-      // the list is streamed once per step: evict-first keeps the gathered
-      // position shadow resident in L2
+    const int si = min(max(int(pfa.w), 0), ns - 1);
+    constexpr int kPre = 4;   // ELL4 blocks requested up front (16 entries)
+    int4 e[kPre];
+    // streamed once per step: evict-first keeps the gathered shadow in L2
+#pragma unroll
+    for (int b = 0; b < kPre; ++b)
+      if (4 * b < m) e[b] = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(4 * b, at, a.npad)));
+#pragma unroll
+    for (int b = 0; b < kPre; ++b) {
+      if (4 * b >= m) break;
+      keep_block(out, at, a.npad, e[b],
+                 filter_block<MULTI>(a, fb, at, pfa, si, e[b], min(4, m - 4 * b)), w);
+    }
+    for (int s0 = 4 * kPre; s0 < m; s0 += 4) {
       const int4 q = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(s0, at, a.npad)));
-      int bb[kDepth] = {q.x, s0 + 1 < m ? q.y : -1, s0 + 2 < m ? q.z : -1,
-                        s0 + 3 < m ? q.w : -1};
-      float4 pb[kDepth];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) pb[u] = a.posf[bb[u] >= 0 ? bb[u] : at];
-#pragma unroll
-      for (int u = 0; u < kDepth; ++u) {
-        if (bb[u] < 0) continue;
-        int v = prefilter(pfa, pb[u], a.boxf, lo, hi);
-        if (v == kUnsure) {
-          double dx, dy, dz;
-          displacement(a.pos[at], a.pos[bb[u]], a.box, dx, dy, dz);
-          v = norm_sq_exact(dx, dy, dz) <= rc2 ? kIn : kOut;
-        }
-        if (v == kIn) out[ell_at(w++, at, a.npad)] = bb[u];
-      }
+      keep_block(out, at, a.npad, q, filter_block<MULTI>(a, fb, at, pfa, si, q, min(4, m - s0)), w);
     }
   } else {
     for (int s = 0; s < m; ++s) out[ell_at(s, at, a.npad)] = skin[ell_at(s, at, a.npad)];
     w = m;
   }
   out_cnt[at] = w;
-  warp_atomic_max(max_count, w);
-  // occupancy histogram for the force kernel's group width (after rebuilds
-  // only): hist[0] = atoms with more than 4 short neighbours, hist[1] = more than 8
-  if (hist) {
+  // largest count and occupancy histogram for the force kernel's group width,
+  // after rebuilds only (same-address atomics from every warp are not free):
+  // hist[0] = atoms with more than 4 short neighbours, hist[1] = more than 8
+  if (max_count) {
+    warp_atomic_max(max_count, w);
     const unsigned act = __activemask();
     const int c4 = __popc(__ballot_sync(act, w > 4)), c8 = __popc(__ballot_sync(act, w > 8));
     if ((threadIdx.x & 31) == __ffs(act) - 1) {
@@ -441,21 +512,43 @@ void snapshot_reference_positions(Ctx& c) {
                            cudaMemcpyDeviceToDevice, c.stream));
 }
 
-void list_filter(Ctx& c, double r_cut_max, bool apply) {
+void list_filter(Ctx& c, FilterMode mode) {
   ListState& s = c.short_list;
   s.cap = c.skin_list.cap;
   s.nbr.reserve(std::size_t(s.cap) * c.npad + 1);
   s.cnt.reserve(std::size_t(c.npad) + 1);
-  const bool reread = c.short_max_stale || c.short_apply != int(apply);
+  const bool reread = c.short_max_stale || c.short_apply != int(mode);
   if (reread) {
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 8, 0, 2 * sizeof(int), c.stream));
   }
+  PairBounds pb{};
+  if (mode != FilterMode::Copy) {
+    const int ns = c.params.species_count();
+    pb.ns = ns;
+    const double rc = c.params.r_cut_max();
+    for (int i = 0; i < ns; ++i)
+      for (int k = 0; k < ns; ++k) {
+        double c2 = rc * rc, cut = rc;   // the reference's test (neighbor.cpp:146)
+        if (mode == FilterMode::Pair) {
+          c2 = 0;
+          for (int j = 0; j < ns; ++j) {
+            const double cc = c.params.entry(i, j, k).cutoff();
+            c2 = std::max(c2, cc * cc);   // the force kernel's cutsq values
+          }
+          cut = std::sqrt(c2);
+        }
+        pb.c2[i * ns + k] = c2;
+        pb.cut[i * ns + k] = cut;
+      }
+  } else {
+    pb.ns = 1;
+  }
   if (c.n > 0) {
-    k_filter<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
-        list_args(c), r_cut_max, r_cut_max * r_cut_max, apply ? 1 : 0, c.skin_list.nbr.get(),
-        c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), c.flags.get() + 4,
-        reread ? c.flags.get() + 8 : nullptr);
+    (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+        list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
+        c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
+        c.flags.get() + 8);
     ++c.launches;
   }
   s.valid = true;
@@ -470,7 +563,7 @@ void list_filter(Ctx& c, double r_cut_max, bool apply) {
     s.over4 = f[8];
     s.over8 = f[9];
     c.short_max_stale = false;
-    c.short_apply = int(apply);
+    c.short_apply = int(mode);
   }
 }
 
