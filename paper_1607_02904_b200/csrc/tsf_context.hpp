@@ -100,13 +100,15 @@ struct Ctx {
   // force scratch
   DevBuf<double> px, py, pz;   // deterministic slot buffers [cap * npad]
   DevBuf<double> fself;        // [n][3]
+  DevBuf<double> atom_ev;      // deterministic tier launches: [n][8] energy + virial
   DevBuf<double> partials;     // [blocks][kRedWidth]
   DevBuf<double> result;       // energy + virial (7), reduced
-  DevBuf<int> flags;           // [0] error bits, [1] overflow count, [2] rebuild flag,
+  DevBuf<int> flags;           // [0] error bits, [1]/[2] tier queue counts (force path;
+                               // [2] doubles as the rebuild flag, read synchronously),
                                // [3] largest skin count, [4] largest short count,
                                // [5] |coord| max bits, [6] max cell occupancy,
                                // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
-  DevBuf<int> overflow;        // atoms with more short neighbors than the group width
+  DevBuf<int> overflow;        // [2n] tier queues: atoms over the group width / over 16
 
   // MD state
   DevBuf<double> vel;          // [n][3]

@@ -22,18 +22,21 @@
 //     deterministic mode: P_l goes to a slot buffer and k_gather sums every
 //     atom's incoming slots in list order — bitwise reproducible;
 //   * energy and virial (W_ab = sum_l d_a P_b) are reduced per block into a
-//     partials array and summed in fixed order: deterministic in both modes.
+//     partials array and summed in fixed order; atoms taken by the tier
+//     launches (queued in atomic order) keep theirs per atom in deterministic
+//     mode, summed in atom order by k_queued_ev — bitwise reproducible.
 // The grid is persistent (occupancy x 148 blocks striding over atom tiles)
 // and software-pipelined: while tile k computes, the positions of tile k+1
 // and the list entries of tile k+2 are already in flight (the dependent
 // count -> index -> position loads were 35% of the stall samples, ncu).
 // Atoms whose short count exceeds G are queued and processed by the same code
-// with G = 32 (one warp per atom) in a second launch that exits at once when
-// the queue is empty.
+// in tier launches — G = 16 (two atoms per warp), then G = 32 for what is
+// left — that exit at once when their queue is empty.
 #pragma once
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -66,8 +69,14 @@ struct ForceArgs {
   void* fself;         // deterministic mode: Acc[n][3]
   double* partials;    // [blocks][kRedWidth]
   int partial_base;
-  int* overflow;       // queued atom ids
-  int* flags;          // [0] error bits, [1] overflow count
+  // Atoms with more short entries than the group width are queued for a
+  // wider tier launch (main G=4/8 -> G=16 -> G=32); the last tier flags them.
+  const int* ovf_in;        // tier launches: queued slots and their count
+  const int* ovf_in_count;
+  int* ovf_out;             // nullptr: more than G entries is an error
+  int* ovf_out_count;
+  double* atom_ev;          // deterministic tiers: per-atom energy + virial [n][8]
+  int* flags;               // [0] error bits
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -184,7 +193,7 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
   Acc e_acc = 0;
   Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
 
-  const int n_ovf = OVF ? a.flags[1] : 0;
+  const int n_ovf = OVF ? *a.ovf_in_count : 0;
   if (OVF && n_ovf == 0) {              // nothing queued: leave a zero partial
     if (tid < kRedWidth)
       a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
@@ -224,6 +233,7 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     return t;
   };
 
+  constexpr int kPerWarp = 32 / G;     // tier launches: queued atoms per warp
   int work = OVF ? blockIdx.x * (kBlock / 32) + tid / 32 : blockIdx.x;
   TileIdx nxt{0, 0, 0}, nxt2{0, 0, 0};
   double4 pi_n = make_double4(0, 0, 0, 0), pj_n = pi_n;
@@ -239,10 +249,11 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     double4 pi, pj;
     bool active;
     if (OVF) {
-      if (work >= n_ovf) break;        // warp-uniform
-      i = a.overflow[work];
-      active = true;
-      n_i = a.cnt[i];
+      if (work * kPerWarp >= n_ovf) break;   // warp-uniform
+      const int q = work * kPerWarp + lane / G;
+      active = q < n_ovf;
+      i = a.ovf_in[active ? q : work * kPerWarp];
+      n_i = active ? a.cnt[i] : 0;
       j = gl < n_i ? a.nbr[ell_at(gl, i, a.npad)] : i;
       pi = a.pos[i];
       pj = a.pos[j];
@@ -271,8 +282,8 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     }
     if (n_i > G) {
       if (gl == 0) {
-        if (OVF) atomicOr(a.flags, kErrShortOverflow);
-        else a.overflow[atomicAdd(a.flags + 1, 1)] = i;
+        if (a.ovf_out) a.ovf_out[atomicAdd(a.ovf_out_count, 1)] = i;
+        else atomicOr(a.flags, kErrShortOverflow);
       }
       n_i = 0;
       active = false;
@@ -419,15 +430,33 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
       fz += __shfl_xor_sync(kFull, fz, o);
     }
 
-    if (slot) {
-      e_acc += Acc(v);
+    if constexpr (OVF && DET) {
+      // queue order (and so the block) varies run to run: keep this atom's
+      // energy and virial per atom; k_queued_ev sums them in atom order
       const R rx = R(dx), ry = R(dy), rz = R(dz);
-      w_acc[0] += Acc(rx * px);
-      w_acc[1] += Acc(ry * py);
-      w_acc[2] += Acc(rz * pz);
-      w_acc[3] += Acc(rx * py);
-      w_acc[4] += Acc(rx * pz);
-      w_acc[5] += Acc(ry * pz);
+      Acc ev[7] = {Acc(v), Acc(rx * px), Acc(ry * py), Acc(rz * pz),
+                   Acc(rx * py), Acc(rx * pz), Acc(ry * pz)};
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        if (!slot) ev[q] = Acc(0);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) ev[q] += __shfl_xor_sync(kFull, ev[q], o);
+      }
+      if (active && gl == 0)
+#pragma unroll
+        for (int q = 0; q < 7; ++q) a.atom_ev[8 * std::size_t(i) + q] = double(ev[q]);
+    }
+    if (slot) {
+      if constexpr (!(OVF && DET)) {
+        e_acc += Acc(v);
+        const R rx = R(dx), ry = R(dy), rz = R(dz);
+        w_acc[0] += Acc(rx * px);
+        w_acc[1] += Acc(ry * py);
+        w_acc[2] += Acc(rz * pz);
+        w_acc[3] += Acc(rx * py);
+        w_acc[4] += Acc(rx * pz);
+        w_acc[5] += Acc(ry * pz);
+      }
       if (DET) {
         const std::size_t q = std::size_t(gl) * a.npad + i;
         static_cast<Acc*>(a.slot_x)[q] = Acc(px);
@@ -492,6 +521,36 @@ __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ parti
     __syncthreads();
   }
   if (t < 7) out[t] = s[0][t];
+}
+
+// Deterministic mode: energy + virial of the atoms the tier launches took,
+// summed in atom order (block b owns a fixed contiguous chunk) into the
+// block partials.  "Queued" repeats the main kernel's rule: an owned,
+// non-ghost slot with more short entries than the main width.
+__global__ void __launch_bounds__(kBlock) k_queued_ev(const double* __restrict__ atom_ev,
+                                                      const int* __restrict__ cnt,
+                                                      const int* __restrict__ perm, int n_owned,
+                                                      int center_limit, int g,
+                                                      const int* __restrict__ queued,
+                                                      double* __restrict__ partials) {
+  __shared__ double s[kBlock][7];
+  const int t = threadIdx.x;
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  if (*queued > 0) {
+    const int chunk = (n_owned + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * chunk, hi = min(n_owned, lo + chunk);
+    for (int i = lo + t; i < hi; i += kBlock)
+      if (cnt[i] > g && (perm ? perm[i] : i) < center_limit)
+        for (int q = 0; q < 7; ++q) acc[q] += atom_ev[8 * std::size_t(i) + q];
+  }
+  for (int q = 0; q < 7; ++q) s[t][q] = acc[q];
+  __syncthreads();
+  for (int w = kBlock / 2; w > 0; w >>= 1) {
+    if (t < w)
+      for (int q = 0; q < 7; ++q) s[t][q] += s[t + w][q];
+    __syncthreads();
+  }
+  if (t < kRedWidth) partials[std::size_t(blockIdx.x) * kRedWidth + t] = t < 7 ? s[0][t] : 0.0;
 }
 
 // Deterministic scatter: F_a = F_self(a) + sum over a's short neighbours b of
@@ -586,7 +645,7 @@ int persistent_blocks(K kernel, int tiles) {
   return std::max(1, std::min(tiles, per_sm * sms));
 }
 
-constexpr int kOverflowBlocks = 148;
+constexpr int kOverflowBlocks = 4 * 148;   // per tier launch; idle tiers exit at once
 
 template <typename R, typename Acc, int G, int SPEC, bool DET>
 int launch_main(Ctx& c, ForceArgs<R> a) {
@@ -603,17 +662,30 @@ int launch_main(Ctx& c, ForceArgs<R> a) {
 
 template <typename R, typename Acc, int SPEC, bool DET>
 void run_force(Ctx& c, ForceArgs<R> a) {
-  // Group width from the largest short count seen at the last list build;
-  // atoms that outgrow it between rebuilds take the overflow launch.
-  // The group width covers (nearly) every atom; up to 1-2% of atoms may take
-  // the one-warp-per-atom overflow launch instead of widening every group
-  // (liquid Si: 3-11 neighbours, 97.5% have <= 8).
+  // Group width from the short-count distribution of the last list build
+  // (atoms over 4 / over 8); atoms over the width — or that outgrow it
+  // between rebuilds — take the G=16 / G=32 tier launches.  Measured per-atom
+  // costs (B200, f64; profiles/r01): main G=4 0.26 ns, G=8 0.69 ns, G=16
+  // 1.7 ns (no register cache of d zeta/d x_k above 8), a queued atom
+  // 2.3-2.6 ns, so G=4 wins below ~15% over-4 atoms and G=8 below ~35%
+  // over-8 (3C-SiC 256k: 45% / 8% -> G=8, 1.8x over G=16; liquid Si
+  // 512k -> G=8, 2.0x).
   const ListState& s = c.short_list;
   const int mx = std::max(1, s.max_count);
   const std::int64_t n = std::max<std::int64_t>(c.n, 1);
-  const int g = (mx <= 4 || s.over4 * 100 <= n) ? 4
-                : (mx <= 8 || s.over8 * 50 <= n) ? 8
-                : mx <= 16 ? 16 : 32;
+  int g = (mx <= 4 || s.over4 * 100 <= 15 * n) ? 4
+          : (mx <= 8 || s.over8 * 100 <= 35 * n) ? 8
+          : 16;
+  // TSF_GROUP_WIDTH=4|8|16|32 pins the width (tuning and the tier tests)
+  const char* pin = std::getenv("TSF_GROUP_WIDTH");
+  const int pinned = pin ? std::atoi(pin) : 0;
+  if (pinned == 4 || pinned == 8 || pinned == 16 || pinned == 32) g = pinned;
+  // queues: [0, n) atoms over the main width, [n, 2n) atoms over 16;
+  // counts in flags[1] / flags[2] (zeroed with the error bits per evaluation)
+  int* q1 = c.overflow.get();
+  int* q2 = q1 + c.n;
+  a.ovf_out = g < 32 ? q1 : nullptr;
+  a.ovf_out_count = a.flags + 1;
   int nb = 0;
   switch (g) {
     case 4: nb = launch_main<R, Acc, 4, SPEC, DET>(c, a); break;
@@ -621,10 +693,39 @@ void run_force(Ctx& c, ForceArgs<R> a) {
     case 16: nb = launch_main<R, Acc, 16, SPEC, DET>(c, a); break;
     default: nb = launch_main<R, Acc, 32, SPEC, DET>(c, a); break;
   }
-  a.partial_base = nb;
-  k_force<R, Acc, 32, SPEC, DET, true><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
-  k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb + kOverflowBlocks, c.result.get());
-  c.launches += 2;
+  // The G=16 tier runs only when atoms were over the width at the last
+  // rebuild; otherwise the queue holds the few that outgrew it since, and
+  // the G=32 tier alone takes them (an idle launch still costs ~3 us).
+  const bool tier16 = g < 16 && mx > g;
+  if (tier16) {
+    a.partial_base = nb;
+    a.ovf_in = q1;
+    a.ovf_in_count = a.flags + 1;
+    a.ovf_out = q2;
+    a.ovf_out_count = a.flags + 2;
+    k_force<R, Acc, 16, SPEC, DET, true><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
+    nb += kOverflowBlocks;
+    ++c.launches;
+  }
+  if (g < 32) {
+    a.partial_base = nb;
+    a.ovf_in = tier16 ? q2 : q1;
+    a.ovf_in_count = a.flags + (tier16 ? 2 : 1);
+    a.ovf_out = nullptr;
+    const int blocks32 = g == 16 ? kOverflowBlocks : kOverflowBlocks / 4;
+    k_force<R, Acc, 32, SPEC, DET, true><<<blocks32, kBlock, 0, c.stream>>>(a);
+    nb += blocks32;
+    ++c.launches;
+    if (DET) {
+      k_queued_ev<<<kOverflowBlocks, kBlock, 0, c.stream>>>(
+          a.atom_ev, a.cnt, a.perm, a.n_owned, a.center_limit, g, a.flags + 1,
+          a.partials + std::size_t(nb) * kRedWidth);
+      nb += kOverflowBlocks;
+      ++c.launches;
+    }
+  }
+  k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb, c.result.get());
+  ++c.launches;
 }
 
 template <typename R, typename Acc, bool DET>
@@ -657,11 +758,10 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.cutsq = c.cutsq.get();
   a.ns = c.params.species_count();
   a.flags = c.flags.get();
-  c.overflow.reserve(std::max<std::size_t>(n, 1));
-  a.overflow = c.overflow.get();
-  c.partials.reserve(std::size_t(32 * 148 + kOverflowBlocks + 8) * kRedWidth);
+  c.overflow.reserve(std::max<std::size_t>(2 * n, 1));
+  c.partials.reserve(std::size_t(32 * 148 + 3 * kOverflowBlocks + 8) * kRedWidth);
   a.partials = c.partials.get();
-  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 2 * sizeof(int), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 3 * sizeof(int), c.stream));
 
   constexpr bool kF32 = std::is_same<Acc, float>::value;
   if (det) {
@@ -674,6 +774,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     a.slot_y = c.py.get();
     a.slot_z = c.pz.get();
     a.fself = c.fself.get();
+    c.atom_ev.reserve(8 * n + 1);
+    a.atom_ev = c.atom_ev.get();
     dispatch_spec<R, Acc, true>(c, a);
     if (n > 0) {
       k_gather<Acc><<<ceil_div(n, kBlock), kBlock, 0, c.stream>>>(

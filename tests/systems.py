@@ -87,3 +87,24 @@ def slab_mixed(tb):
     xyz[:, :2] = np.mod(xyz[:, :2], s.box.lengths[:2])
     return Case("slab_xy", xyz, s.species, s.box.lengths, np.array([1, 1, 0], np.uint8), 0.8,
                 si_text(tb))
+
+
+def dense_random(tb, n=1200, density=0.14, dmin=1.5, seed=21, skin=0.5):
+    """Random sequential packing (no pair closer than dmin) at ~2x the
+    crystal density: 3..25 short neighbours per atom, so every lane-group
+    tier (4 -> 16 -> 32) carries atoms."""
+    rng = np.random.default_rng(seed)
+    box = np.full(3, (n / density) ** (1.0 / 3.0))
+    pts = np.empty((n, 3))
+    m = 0
+    while m < n:
+        p = rng.uniform(0.0, box)
+        if m:
+            d = pts[:m] - p
+            d -= box * np.round(d / box)
+            if (d * d).sum(axis=1).min() < dmin * dmin:
+                continue
+        pts[m] = p
+        m += 1
+    return Case(f"dense_random{n}", pts, np.zeros(n, np.int32), box, np.ones(3, np.uint8), skin,
+                si_text(tb))

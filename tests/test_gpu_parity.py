@@ -301,3 +301,40 @@ def test_large_n_against_compensated_oracle(tb, oracle):
         e, f, _ = ctx.compute(prec)
         assert abs(e - ref["energy_ld"]) <= E_TOL_M * abs(ref["energy_ld"])
         assert np.abs(f - ref["forces"]).max() <= F_TOL_M * max(1, np.abs(ref["forces"]).max())
+
+
+@pytest.mark.parametrize("width", ["4", "8", "16", "32"])
+def test_group_width_tiers(tb, oracle, monkeypatch, width):
+    """Pinned main group width on a dense packing (8..21 short neighbours):
+    atoms over the width go through the G=16 and G=32 tier launches; every
+    width gives the oracle's energy, forces and virial."""
+    monkeypatch.setenv("TSF_GROUP_WIDTH", width)
+    case = systems.dense_random(tb)
+    params, ctx = _ctx(tb, case)
+    _, _, _, ref = _oracle(oracle, case, params)
+    fscale = max(1.0, np.abs(ref["forces"]).max())
+    for det in (True, False):
+        e, f, w = ctx.compute("double", deterministic=det)
+        assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D * fscale
+        assert np.abs(w - ref["virial"]).max() <= 1e-10 * max(1.0, np.abs(ref["virial"]).max())
+        e, f, _ = ctx.compute("single", deterministic=det)
+        assert abs(e - ref["energy"]) <= E_TOL_M * abs(ref["energy"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_M * fscale
+    ctx.close()
+
+
+def test_short_export_keeps_reference_filter(tb, oracle, sic_text):
+    """The force path filters SiC pairs by their species-pair cutoff; the
+    exported short list stays the reference's r_cut_max list
+    (neighbor.cpp:143-180) before and after a force evaluation."""
+    case = systems.zincblende(tb, sic_text, 4, jitter=0.1, seed=1, skin=0.5)
+    params, ctx = _ctx(tb, case)
+    ooff, onb = oracle.build_neighbor_list(case.xyz, case.box, case.periodic, params.r_cut_max,
+                                           case.skin)
+    xoff, xnb = oracle.filter(case.xyz, case.box, case.periodic, ooff, onb, params.r_cut_max)
+    for _ in range(2):
+        ctx.compute("double")
+        soff, snb = ctx.export_neighbors("short")
+        assert np.array_equal(soff, xoff) and np.array_equal(snb, xnb)
+    ctx.close()
