@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "tsf_context.hpp"
@@ -150,24 +151,22 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
   const R arg = ok ? p.lam3 * (j.r - k.r) : R(0);
   const bool cubic = p.m3 != R(0);
   const R ex = Fn<R>::exp_(cubic ? arg * arg * arg : arg);
-  const R dex = ex * p.lam3 * (cubic ? R(3) * arg * arg : R(1));
-  const R fg = fck * g;
-  o.z = fg * ex;
-  const R fgd = fck * dg * ex;
-  const R fge = fg * dex;
-  const R cge = dfck * g * ex;
-  // d cos / d x_j and d cos / d x_k
-  const R gjx = (k.ux - j.ux * cs) * j.ir, gjy = (k.uy - j.uy * cs) * j.ir,
-          gjz = (k.uz - j.uz * cs) * j.ir;
-  const R gkx = (j.ux - k.ux * cs) * k.ir, gky = (j.uy - k.uy * cs) * k.ir,
-          gkz = (j.uz - k.uz * cs) * k.ir;
-  o.jx = gjx * fgd + j.ux * fge;
-  o.jy = gjy * fgd + j.uy * fge;
-  o.jz = gjz * fgd + j.uz * fge;
-  const R ck = cge - fge;
-  o.kx = k.ux * ck + gkx * fgd;
-  o.ky = k.uy * ck + gky * fgd;
-  o.kz = k.uz * ck + gkz * fgd;
+  const R gx = g * ex;
+  o.z = fck * gx;
+  const R fge = o.z * (cubic ? R(3) * p.lam3 * (arg * arg) : p.lam3);   // dz/dr_ij via exp
+  const R fgd = fck * dg * ex;                                          // dz/dcos
+  const R cge = dfck * gx;                                              // dz/dr_ik via f_C
+  // dcos/dx_j = (u_k - u_j cos)/r_ij, dcos/dx_k = (u_j - u_k cos)/r_ik, folded:
+  //   dz/dx_j = u_k A + u_j (fge - cos A),             A = fgd / r_ij
+  //   dz/dx_k = u_j C + u_k (cge - fge - cos C),       C = fgd / r_ik
+  const R A = fgd * j.ir, B = fge - cs * A;
+  o.jx = k.ux * A + j.ux * B;
+  o.jy = k.uy * A + j.uy * B;
+  o.jz = k.uz * A + j.uz * B;
+  const R C = fgd * k.ir, D = (cge - fge) - cs * C;
+  o.kx = j.ux * C + k.ux * D;
+  o.ky = j.uy * C + k.uy * D;
+  o.kz = j.uz * C + k.uz * D;
   return o;
 }
 
@@ -177,10 +176,36 @@ struct TileIdx {
   int i, n, j;
 };
 
+// Resident blocks per SM the register allocation must allow (B200, si2m /
+// liquid512k sweeps): FP64 4 (128 registers; unbounded it takes 168 and
+// runs 12% slower, 5+ blocks spill), float 6 (80 registers, +5%).
+#ifndef TSF_FORCE_MINB_F64
+#define TSF_FORCE_MINB_F64 4
+#endif
+#ifndef TSF_FORCE_MINB_F32
+#define TSF_FORCE_MINB_F32 6
+#endif
+#ifndef TSF_FORCE_MINB_F64_G8
+#define TSF_FORCE_MINB_F64_G8 TSF_FORCE_MINB_F64
+#endif
+#ifndef TSF_FORCE_MINB_F32_G8
+#define TSF_FORCE_MINB_F32_G8 5   // unrolled G = 8 cache: 96 registers, no spills
+#endif
+template <typename R, int G>
+constexpr int kForceMinBlocks = G == 8 ? TSF_FORCE_MINB_F64_G8 : TSF_FORCE_MINB_F64;
+template <int G>
+constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_FORCE_MINB_F32;
+
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF>
-__global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceArgs<R> a) {
+__global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
+    k_force(const __grid_constant__ ForceArgs<R> a) {
   constexpr bool kCache = G <= 8;     // register cache of d zeta / d x_k
-  constexpr int kUnroll = kCache ? G : 2;
+  constexpr int kUnroll = kCache ? G - 1 : 2;   // the trip count: full unroll keeps the cache in registers
+  // FP64, G = 8: early exit at the warp's largest count keeps the loop rolled
+  // and the cache in (L1-backed) local memory, which measured 2-6% faster
+  // than the unrolled, register-capped form; float unrolls (liquid512k /
+  // sic256k sweeps, profiles/r01)
+  constexpr bool kRolled = G == 8 && std::is_same<R, double>::value;
   constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
   __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
   __shared__ double scut[SPEC == kSingle ? 1 : kRows];
@@ -327,7 +352,10 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     R ckx[kCache ? G : 1], cky[kCache ? G : 1], ckz[kCache ? G : 1];
 #pragma unroll kUnroll
     for (int t = 1; t < G; ++t) {
-      if (G > 4 && t >= tmax) break;   // warp-uniform
+      if (G > 4 && t >= tmax) {           // warp-uniform
+        if (kRolled) break;
+        continue;
+      }
       int m = gl + t;
       if (m >= n_i) m -= n_i;
       const int src = gbase + (m & (G - 1));
@@ -382,7 +410,10 @@ __global__ void __launch_bounds__(kBlock) k_force(const __grid_constant__ ForceA
     // is zero unless t < n_i and its triplet counts, so receivers need no mask.
 #pragma unroll kUnroll
     for (int t = 1; t < G; ++t) {
-      if (G > 4 && t >= tmax) break;   // warp-uniform
+      if (G > 4 && t >= tmax) {           // warp-uniform
+        if (kRolled) break;
+        continue;
+      }
       R sx, sy, sz;
       if constexpr (kCache) {
         sx = ckx[t] * dvdz;
