@@ -115,20 +115,37 @@ struct PairBounds {
   int ns;
 };
 
-__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const BoxF& box,
-                                         float lo, float hi) {
-  float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
-  // one conditional +-L per periodic axis, as selects (no branches); the
-  // choice is made on the unwrapped d, exactly as "if d > h: d -= L elif
-  // d < -h: d += L"
+// Per-thread wrap constants for the float pre-test: 1/L = 0 on open axes.
+struct WrapF {
+  float inv[3], l[3];
+};
+
+__device__ __forceinline__ WrapF wrap_of(const BoxF& box) {
+  WrapF w;
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
-    const float h = box.per[ax] ? box.half[ax] : __int_as_float(0x7f800000);
-    const float dm = d[ax] - box.len[ax], dp = d[ax] + box.len[ax];
-    d[ax] = d[ax] > h ? dm : (d[ax] < -h ? dp : d[ax]);
+    w.inv[ax] = box.per[ax] ? 1.0f / box.len[ax] : 0.0f;
+    w.l[ax] = box.len[ax];
   }
+  return w;
+}
+
+__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const WrapF& w,
+                                         float lo, float hi) {
+  float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+  // float minimum image d - L rint(d / L) (3 instructions per axis).  It can
+  // pick the other image than the exact test only at |d| ~ L/2, where both
+  // images have the same length up to rounding — inside the error band, so
+  // such a pair takes the exact FP64 test.
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) d[ax] = fmaf(-w.l[ax], rintf(d[ax] * w.inv[ax]), d[ax]);
   const float r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
   return r2 < lo ? kIn : (r2 > hi ? kOut : kUnsure);
+}
+
+__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const BoxF& box,
+                                         float lo, float hi) {
+  return prefilter(a, b, wrap_of(box), lo, hi);
 }
 
 
