@@ -47,6 +47,12 @@ CONFIGS = {
                    "(2 ps) and held at 3000 K (4 ps), dt 0.5 fs, velocity rescaling every 50 "
                    "steps (SURVEY.md 8d)"),
 }
+# --impl reference / cpu_baseline: the same workload (lattice, jitter, skin,
+# parameters) at a bounded size, so a --steps K run of the reference's CPU
+# path ends within minutes (the path is O(N): atom-steps/s is size-independent)
+REF_SAMPLE_CELLS = {"si2m": (40, 40, 10), "si32k": (20, 20, 10), "sic256k": (20, 20, 20),
+                    "liquid512k": (25, 25, 25)}
+REF_TIME_CAP_S = 240.0
 DTYPES = {"double": "f64", "mixed": "f32 compute / f64 accumulate", "single": "f32"}
 REF_OPTS = {"double": ("v1", "opt-d", 4), "mixed": ("v2", "opt-m", 8),
             "single": ("v2", "opt-s", 8)}
@@ -57,12 +63,13 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_system(cfg: str):
+def make_system(cfg: str, cells=None):
     """Synthetic input of the workload: diamond (or zincblende) lattice with a
-    seeded uniform thermal-like jitter (positions wrapped into the box)."""
+    seeded uniform thermal-like jitter (positions wrapped into the box);
+    `cells` overrides the size (the reference arm's bounded sample)."""
     import paper_1607_02904_b200 as tb
-    cells, a0, jitter, pkind, _ = CONFIGS[cfg]
-    s = tb.make_diamond_lattice(*cells, a0)
+    full_cells, a0, jitter, pkind, _ = CONFIGS[cfg]
+    s = tb.make_diamond_lattice(*(cells or full_cells), a0)
     rng = np.random.default_rng(12345)
     xyz = np.mod(s.positions + rng.uniform(-jitter, jitter, s.positions.shape), s.box.lengths)
     if cfg.startswith("liquid"):
@@ -114,9 +121,12 @@ def algorithmic_work(xyz, species, box, offsets, nbrs, rows, ns):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons during the timed region: the
+    sampler runs from before the warm-up; only samples stamped inside the
+    timed window [t_lo, t_hi] (host wall clock) are kept (the nearest later
+    one if the window is shorter than the 50 ms sampling period)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -129,31 +139,45 @@ class ClockSampler:
         except OSError:
             self.p = None
 
-    def stop(self):
+    @staticmethod
+    def _stamp(text: str):
+        import datetime
+        try:
+            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
+    def stop(self, t_lo: float, t_hi: float):
         if self.p is None:
             return None
-        time.sleep(0.25)
+        time.sleep(0.12)
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         rows = []
         for line in open(self.f.name):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 7:
-                rows.append(parts)
+            if len(parts) == 8:
+                rows.append((self._stamp(parts[0]), parts[1:]))
         os.unlink(self.f.name)
-        if not rows:
+        inside = [r for ts, r in rows if ts is not None and t_lo <= ts <= t_hi]
+        if not inside:
+            later = [r for ts, r in rows if ts is not None and ts >= t_lo]
+            inside = later[:1] or [r for _, r in rows][-1:]
+        if not inside:
             return None
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in inside if r[0].replace(".", "").isdigit()]
         reasons = set()
-        for r in rows:
+        for r in inside:
             for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                                 "sw_power_cap"), r[3:]):
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "samples": len(rows), "reasons": sorted(reasons)}
+                "sm_max_mhz": float(inside[0][1]) if inside[0][1].replace(".", "").isdigit()
+                else None,
+                "samples": len(inside), "window_s": round(t_hi - t_lo, 3),
+                "reasons": sorted(reasons)}
 
 
 def load_peak(precision: str):
@@ -170,7 +194,11 @@ def load_traffic(cfg: str, precision: str, det: bool):
     if not os.path.exists(path):
         return None
     tab = json.load(open(path))
-    return tab.get(f"{cfg}/{precision}/{'det' if det else 'atomic'}")
+    ent = tab.get(f"{cfg}/{precision}/{'det' if det else 'atomic'}") or {}
+    force = ent.get("force")
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch of the main force
+    # kernel (ncu, tools/ncu_traffic.sh -> profiles/ncu_traffic.json)
+    return force["traffic_bytes"] if force else None
 
 
 def run_reference(args):
@@ -185,28 +213,34 @@ def run_reference(args):
                           "oracle/_ref/libtmdref.so not built (run __graft_entry__.build())"}))
         return
     R = Reference()
-    text, xyz, species, box, per, masses = make_system(args.config)
+    text, xyz, species, box, per, masses = make_system(args.config, REF_SAMPLE_CELLS[args.config])
     n = len(xyz)
     ph = R.params(text)
     sh = R.system(xyz, species, masses, box, per)
     lh = R.neighbor_list(sh, R.lib.tmdref_params_r_cut_max(ph), 1.0)
     scheme, prec, width = REF_OPTS[args.precision]
     cores = os.cpu_count() or 1
+    tw = time.perf_counter()
     for _ in range(args.warmup):
         R.evaluate(sh, lh, ph, n, scheme, prec, width, 16, cores, True, with_forces=False)
+    t_step = (time.perf_counter() - tw) / args.warmup
+    timed = min(args.steps, max(1, int(REF_TIME_CAP_S / max(t_step, 1e-9))))
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(timed):
         R.evaluate(sh, lh, ph, n, scheme, prec, width, 16, cores, True, with_forces=False)
     t = time.perf_counter() - t0
-    value = n * args.steps / t
-    sample = (f"evaluate_forces({scheme}, width {width}, {prec}, workers={cores}) on the full "
-              f"{n}-atom system per step")
+    value = n * timed / t
+    sample = (f"evaluate_forces({scheme}, width {width}, {prec}, workers={cores}) per step on "
+              f"a {n}-atom sample of the same workload ({'x'.join(map(str, REF_SAMPLE_CELLS[args.config]))}"
+              f" cells, same jitter and skin); {timed} of {args.steps} steps timed"
+              f"{' (time cap)' if timed < args.steps else ''}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / timed,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": DTYPES[args.precision], "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][4], "precision": args.precision},
+        "config": {"workload": CONFIGS[args.config][4], "precision": args.precision,
+                   "sample_atoms": n},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -234,7 +268,7 @@ def cpu_baseline(text, xyz, species, box, per, masses):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--precision", default="double", choices=list(DTYPES))
     ap.add_argument("--config", default="si2m", choices=list(CONFIGS))
@@ -296,6 +330,7 @@ def main():
             dec.evaluate(args.precision, args.deterministic)
     algo_flop = 75 * P + 143 * T
 
+    clocks = ClockSampler(local)       # running before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -304,20 +339,21 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    clocks = ClockSampler(local)
     l0 = ctx.launches
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    t_lo = time.time()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     e1.synchronize()
     torch.cuda.synchronize()
+    t_hi = time.time()
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(t_lo, t_hi)
     launches = ctx.launches - l0
     t = e0.elapsed_time(e1) / 1e3
     if world > 1:

@@ -1,0 +1,58 @@
+"""Fold gpurun_out/traffic/<cfg>_<precision>.csv (tools/ncu_traffic.sh) into
+profiles/ncu_traffic.json: per config/precision/scatter mode, the mean DRAM
+read+write bytes and duration per launch of the main force kernel and of the
+filter (ncu, one GPU, --clock-control none; cold-cache serialised launches)."""
+import csv
+import glob
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def fold(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    if not rows:
+        return None
+    h = rows[0]
+    per = {}
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        name = d["Kernel Name"]
+        kind = "filter" if "k_filter" in name else "force"
+        e = per.setdefault(d["ID"], {"kind": kind, "name": name})
+        v = float(d["Metric Value"].replace(",", ""))
+        unit = d["Metric Unit"]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3,
+                 "ms": 1e6, "usecond": 1e3, "nsecond": 1, "msecond": 1e6}.get(unit, 1)
+        e[d["Metric Name"]] = v * scale
+    out = {}
+    for kind in ("force", "filter"):
+        ks = [e for e in per.values() if e["kind"] == kind]
+        if not ks:
+            continue
+        rd = sum(e.get("dram__bytes_read.sum", 0) for e in ks) / len(ks)
+        wr = sum(e.get("dram__bytes_write.sum", 0) for e in ks) / len(ks)
+        ns = sum(e.get("gpu__time_duration.sum", 0) for e in ks) / len(ks)
+        out[kind] = {"kernel": ks[0]["name"][:120], "launches": len(ks), "dram_read_bytes": rd,
+                     "dram_write_bytes": wr, "traffic_bytes": rd + wr, "duration_ns": ns}
+    return out
+
+
+def main():
+    src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "traffic")
+    dst = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tab = json.load(open(dst)) if os.path.exists(dst) else {}
+    for path in sorted(glob.glob(os.path.join(src, "*.csv"))):
+        cfg, prec = os.path.basename(path)[:-4].rsplit("_", 1)
+        res = fold(path)
+        if res:
+            tab[f"{cfg}/{prec}/atomic"] = res
+    json.dump(tab, open(dst, "w"), indent=1, sort_keys=True)
+    print(json.dumps({k: {kk: vv.get("traffic_bytes") for kk, vv in v.items()}
+                      for k, v in tab.items()}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,16 +1,17 @@
 # usage: bash tools/ncu_traffic.sh [config...]
-# DRAM bytes per launch of the main force kernel (and the filter) for each
-# config x precision, for bench.py's roofline.traffic (tools/ncu_traffic.py
-# folds the CSVs into profiles/ncu_traffic.json).  One GPU; each bench command
-# is run once without ncu first.
+# DRAM bytes and duration per launch of the main force kernel and the filter
+# for each config x precision (tools/ncu_traffic.py folds the CSVs into
+# profiles/ncu_traffic.json for bench.py's roofline.traffic).  One GPU; each
+# bench command runs once without ncu first.
 CFGS=${@:-si2m}
 mkdir -p gpurun_out/traffic
 for C in $CFGS; do
   for P in double mixed single; do
-    B="python bench.py --config $C --precision $P --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-variants"
+    B="python bench.py --config $C --precision $P --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-variants"
     $B > gpurun_out/traffic/plain_${C}_$P.log 2>&1 || { echo "plain $C $P failed"; continue; }
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        --clock-control none -k regex:"k_force|k_filter" -s 4 -c 4 --csv \
+        --clock-control none --kernel-name-base demangled \
+        -k 'regex:k_force<.*\(bool\)0>|k_filter' -s 4 -c 4 --csv \
         --log-file gpurun_out/traffic/${C}_$P.csv $B > gpurun_out/traffic/ncu_${C}_$P.log 2>&1
     echo "ncu $C $P rc=$?"
   done
