@@ -189,16 +189,24 @@ def load_peak(precision: str):
     return (37.2 if precision == "double" else 74.4), "derived (148 SM x 1.965 GHz x FMA lanes)"
 
 
-def load_traffic(cfg: str, precision: str, det: bool):
+def load_ncu(cfg: str, precision: str, det: bool):
+    """The main force kernel's ncu record for this workload (tools/ncu_traffic.sh
+    -> profiles/ncu_traffic.json): DRAM read + write bytes per launch, and the
+    pipe utilisation (fraction of peak sustained, time-weighted) — the north
+    star's issue-rate view of the same kernel."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
-        return None
+        return None, None
     tab = json.load(open(path))
     ent = tab.get(f"{cfg}/{precision}/{'det' if det else 'atomic'}") or {}
     force = ent.get("force")
-    # dram__bytes_read.sum + dram__bytes_write.sum per launch of the main force
-    # kernel (ncu, tools/ncu_traffic.sh -> profiles/ncu_traffic.json)
-    return force["traffic_bytes"] if force else None
+    if not force:
+        return None, None
+    pipes = force.get("pipes_frac_of_peak")
+    issue = None
+    if pipes:
+        issue = {"source": "ncu, profiles/ncu_traffic.json (tools/ncu_traffic.sh)", **pipes}
+    return force["traffic_bytes"], issue
 
 
 def run_reference(args):
@@ -331,6 +339,9 @@ def main():
     algo_flop = 75 * P + 143 * T
 
     clocks = ClockSampler(local)       # running before the warm-up
+    # NVTX range around the steady state: ncu captures (tools/ncu_*.sh) use
+    # --nvtx-include so input preparation (e.g. the liquid melt) is skipped
+    torch.cuda.nvtx.range_push("bench_steps")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -368,11 +379,13 @@ def main():
         step()
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
+    torch.cuda.nvtx.range_pop()
     calls = max(prof["calls"], 1)
     force_s = prof["force_ms"] / calls / 1e3
     stage_total = prof["filter_ms"] + prof["setup_ms"] + prof["force_ms"] + prof["tail_ms"]
     peak, peak_src = load_peak(args.precision)
     achieved = algo_flop / force_s / 1e12
+    ncu_traffic, ncu_issue = load_ncu(args.config, args.precision, args.deterministic)
 
     # e2e through the drop-in C-ABI call with host buffers
     e2e = None
@@ -502,8 +515,9 @@ def main():
             "roofline": {
                 "bound": "fp64" if args.precision == "double" else "fp32",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.config, args.precision,
-                                                                 args.deterministic),
+                "frac": achieved / peak, "traffic": ncu_traffic,
+                "algo_fraction": achieved / peak,
+                "issue_rate": ncu_issue,
                 "kernel": "k_force (main launch)", "peak_source": peak_src,
                 "algo_flop_per_launch": algo_flop, "pairs": P, "triplets": T,
                 "algo_flop_formula": "75 P + 143 T (SURVEY.md 8d / Appendix A)",

@@ -11,6 +11,20 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+# ncu pipe metrics (.avg.pct_of_peak_sustained_elapsed) -> short names
+PIPES = {
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed": "fp64_cycles",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_elapsed": "fp64_inst",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed": "fma_cycles",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_elapsed": "fma_inst",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_elapsed": "xu_inst",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_elapsed": "alu_inst",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_elapsed": "lsu_inst",
+    "smsp__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput",
+}
+
+
 def fold(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     if not rows:
@@ -24,7 +38,7 @@ def fold(path):
         e = per.setdefault(d["ID"], {"kind": kind, "name": name})
         v = float(d["Metric Value"].replace(",", ""))
         unit = d["Metric Unit"]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3,
+        scale = {"%": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3,
                  "ms": 1e6, "usecond": 1e3, "nsecond": 1, "msecond": 1e6}.get(unit, 1)
         e[d["Metric Name"]] = v * scale
     out = {}
@@ -36,7 +50,15 @@ def fold(path):
         wr = sum(e.get("dram__bytes_write.sum", 0) for e in ks) / len(ks)
         ns = sum(e.get("gpu__time_duration.sum", 0) for e in ks) / len(ks)
         out[kind] = {"kernel": ks[0]["name"][:120], "launches": len(ks), "dram_read_bytes": rd,
-                     "dram_write_bytes": wr, "traffic_bytes": rd + wr, "duration_ns": ns}
+                     "dram_write_bytes": wr, "traffic_bytes": rd + wr, "duration_ns": ns,
+                     "dram_gbps": (rd + wr) / ns if ns else None}
+        pipes = {}
+        for key, short in PIPES.items():
+            vals = [e[key] for e in ks if key in e]
+            if vals:
+                pipes[short] = round(sum(vals) / len(vals) / 100.0, 4)
+        if pipes:
+            out[kind]["pipes_frac_of_peak"] = pipes
     return out
 
 
