@@ -458,7 +458,9 @@ def main():
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
         e2e = {"value": n * world * args.steps / te, "unit": UNIT,
-               "h2d_bytes_per_step": int(hx.numel() * 8),
+               # positions and (page-locked, so re-sent and checked on the
+               # device each call) species in; forces, energy, virial out
+               "h2d_bytes_per_step": int(hx.numel() * 8 + sp_t.numel() * 4),
                "d2h_bytes_per_step": int(hf.numel() * 8 + 8 + 48),
                "ms_per_step": 1e3 * te / args.steps,
                "call": "tsf_evaluate_forces (include/tersoff_b200.h), pinned host buffers"}
