@@ -333,6 +333,10 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     me.uz = R(dz) * me.ir;
     R fc, dfc;
     cutoff_ramp(me.r, pjj, fc, dfc);
+    // the radial pair terms depend on r only: issued before the zeta pass so
+    // their two exp chains overlap it instead of lengthening the pair block
+    const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
+    const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
     // meta: species of this slot as a k, or -1 when it can never be one.
     // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
     // exactly "pair (i, k) inside its own cutoff".
@@ -389,9 +393,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     // ---- pair block (potential.hpp:204-222) ----
     R dvdr = 0, dvdz = 0, v = 0;
     if (pair_ok) {
-      const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
       const R dfr = -pjj.lam1 * fr;
-      const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
       const R dfa = -pjj.lam2 * fa;
       R b, db;
       bond_order(zeta, pjj, b, db);
