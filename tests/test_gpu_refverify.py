@@ -1,0 +1,64 @@
+"""The reference's own verification battery (tmd::run_verification,
+proj/src/verify.cpp:822-845) run against the B200 path: oracle/_ref/refverify_b200
+links the unmodified reference sources with integration/potential_b200.cpp,
+which replaces tmd::evaluate_forces, so every evaluate_forces call of the
+battery — scheme/width equivalence, Newton, filter soundness, precision gap,
+determinism and a 25-step Engine rerun — runs on the GPU.
+
+Expected non-passes, asserted precisely:
+  * kmax_sweep: only its bitwise clauses ("v3 k_max=0 not bitwise", "v3
+    k_max=16 differs from cached scalar path") — bit equality with the CPU's
+    glibc libm is out of reach for any GPU path; its tolerance
+    sweep (1e-12 E, 1e-10 F) must pass;
+  * zeta_gradients on the SiC table: the check exercises the reference's own
+    scalar kern::zeta_term against finite differences (no evaluate_forces
+    call), which misses its 1e-6 gate for SiC's c^2/d^2 = 3.8e7 — a property
+    of the reference, not of this path.
+"""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "refverify_b200")
+BITWISE_NOTES = {"v3 k_max=0 not bitwise", "v3 k_max=16 differs from cached scalar path"}
+
+
+def _run(*args):
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/refverify_b200 not built (needs /root/reference at build time)")
+    p = subprocess.run([BIN, *args], capture_output=True, text=True, timeout=600)
+    rows = {}
+    for line in p.stdout.splitlines():
+        status, name, *detail = line.split(" ", 2)
+        rows[name] = (status, detail[0] if detail else "")
+    assert rows, p.stdout + p.stderr
+    return rows
+
+
+def _check(rows, allowed_fail=()):
+    assert len(rows) == 16
+    for name, (status, detail) in rows.items():
+        if name == "kmax_sweep" and status == "FAIL":
+            notes = {x.strip() for x in detail.split(";") if x.strip()}
+            assert notes <= BITWISE_NOTES, detail
+        elif name in allowed_fail:
+            continue
+        else:
+            assert status == "PASS", (name, detail)
+
+
+def test_reference_battery_silicon():
+    rows = _run()
+    _check(rows)
+    # the GPU path's scheme/width sweep against compute_ref, as the battery measures it
+    assert rows["scheme_equivalence"][0] == "PASS"
+    assert rows["determinism"][0] == "PASS"
+
+
+def test_reference_battery_sic():
+    _check(_run(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")),
+           allowed_fail=("zeta_gradients",))
