@@ -62,3 +62,19 @@ def test_reference_battery_silicon():
 def test_reference_battery_sic():
     _check(_run(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")),
            allowed_fail=("zeta_gradients",))
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.parametrize("criterion", range(1, 9))
+def test_reference_acceptance_gate(criterion):
+    """proj/tests/acceptance.cpp criteria 1-8 with evaluate_forces on the B200
+    (1: single-precision 10^4-step trajectory within 2e-5 of double; 2: every
+    scheme x width x k_max within 1e-12 E / 1e-10 F of compute_ref; 4: 10^4-step
+    NVE — drift < 1e-4, |sum F| < 1e-10, momentum < 1e-8; 5: filter on/off
+    1e-12; 3, 6, 7 are CPU-side; 8 reports ns/day, non-gating)."""
+    if not os.path.exists(ACC):
+        pytest.skip("oracle/_ref/acceptance_b200 not built (needs /root/reference at build time)")
+    p = subprocess.run([ACC, str(criterion)], capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0 and p.stdout.startswith("PASS"), p.stdout + p.stderr
