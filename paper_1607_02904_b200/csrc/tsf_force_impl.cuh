@@ -181,6 +181,7 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
 // then the two positions (stage B, dependent on stage A).
 struct TileIdx {
   int i, n, j;
+  bool ghost;   // a decomposition ghost: receives forces, is not a centre
 };
 
 // Resident blocks per SM the register allocation must allow (B200, si2m /
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   const int ntiles = (a.n_owned + kAtomsPerBlock - 1) / kAtomsPerBlock;
   const int nwarps_total = gridDim.x * (kBlock / 32);
   const int last = a.n_owned - 1;
+  const bool has_ghosts = a.center_limit < a.n_owned;
 
   // stage A loads: count and this lane's list entry (clamped into range; the
   // entry past the count is unused, it only keeps the dependent load legal)
@@ -262,12 +264,15 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     t.n = in ? a.cnt[t.i] : 0;
     const int v = in ? a.nbr[ell_at(gl, t.i, a.npad)] : 0;
     t.j = unsigned(v) <= unsigned(last) ? v : 0;
+    // ghost test two tiles ahead (its perm[] load at the tile start was 24%
+    // of the stall samples, ncu); skipped when the context has no ghosts
+    t.ghost = has_ghosts && in && (a.perm ? a.perm[t.i] : t.i) >= a.center_limit;
     return t;
   };
 
   constexpr int kPerWarp = 32 / G;     // tier launches: queued atoms per warp
   int work = OVF ? blockIdx.x * (kBlock / 32) + tid / 32 : blockIdx.x;
-  TileIdx nxt{0, 0, 0}, nxt2{0, 0, 0};
+  TileIdx nxt{0, 0, 0, false}, nxt2{0, 0, 0, false};
   double4 pi_n = make_double4(0, 0, 0, 0), pj_n = pi_n;
   if (!OVF) {
     nxt = load_idx(work);
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       i = nxt.i;
       n_i = nxt.n;
       j = nxt.j;
+      const bool ghost = nxt.ghost;
       pi = pi_n;
       pj = pj_n;
       // keep the pipeline full: positions of the next tile, list of the one after
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       nxt2 = load_idx(work + 2 * gridDim.x);
       active = work * kAtomsPerBlock + tid / G < a.n_owned;
       // ghost copies (decomposition) receive forces but are not centers
-      if (active && (a.perm ? a.perm[i] : i) >= a.center_limit) {
+      if (active && ghost) {
         if (DET && gl == 0) {
           Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
           f[0] = f[1] = f[2] = Acc(0);

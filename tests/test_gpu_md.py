@@ -48,7 +48,12 @@ def test_nve_energy_conservation(tb, precision, tol):
     e = np.array([x["etot_eV"] for x in rep["samples"]])
     assert np.abs(e - e[0]).max() / abs(e[0]) < tol
     fin = rep["system"]
-    assert np.abs(fin.forces.sum(axis=0)).max() < (1e-10 if precision == "double" else 1e-6)
+    # |sum F|: double 1e-10 (criterion 4's bar); mixed accumulates across atoms
+    # in double (float per-atom partials, ~1e-7); single accumulates in float
+    # by design (OptS), a random walk of ~sqrt(N) 2^-24 |F| ~ 1e-6 over 512
+    # atoms in nondeterministic atomic order — gated at 1e-5
+    fsum_tol = {"double": 1e-10, "mixed": 1e-6, "single": 1e-5}[precision]
+    assert np.abs(fin.forces.sum(axis=0)).max() < fsum_tol
     m = np.asarray(fin.species_masses)[fin.species]
     p = (fin.velocities * m[:, None]).sum(axis=0)
     # float per-atom partials leave |sum F| ~ 1e-7 eV/A: a momentum walk of
