@@ -526,7 +526,8 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
       if (len < 0) throw tsf::ConfigError("neighbor offsets must be non-decreasing");
       mx = std::max(mx, len);
     }
-    const int cap = std::max(4, (mx + 3) / 4 * 4);
+    // >= 16 entries: the filter reads the first 4 ELL4 rows unconditionally
+    const int cap = std::max(16, (mx + 3) / 4 * 4);
     std::vector<int> ell(std::size_t(cap) * c.npad, 0), cnt(std::size_t(c.npad), 0);
     for (std::int64_t a = 0; a < c.n; ++a) {
       cnt[std::size_t(a)] = offsets[a + 1] - offsets[a];

@@ -288,11 +288,13 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     const int si = min(max(int(pfa.w), 0), ns - 1);
     constexpr int kPre = 4;   // ELL4 blocks requested up front (16 entries)
     int4 e[kPre];
-    // streamed once per step: evict-first keeps the gathered shadow in L2
+    // streamed once per step: evict-first keeps the gathered shadow in L2.
+    // Loaded without waiting for the count (every list has >= 16 allocated
+    // entries; those past the count are masked off in test_block), so count
+    // and list cost one DRAM round trip, not two.
 #pragma unroll
     for (int b = 0; b < kPre; ++b)
-      e[b] = 4 * b < m ? __ldcs(reinterpret_cast<const int4*>(skin + ell_at(4 * b, at, a.npad)))
-                       : make_int4(at, at, at, at);
+      e[b] = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(4 * b, at, a.npad)));
     // test all 16 before any store or exact fallback: nothing between the
     // gathers keeps the compiler from issuing them back to back
     unsigned keep = 0, uns = 0;
