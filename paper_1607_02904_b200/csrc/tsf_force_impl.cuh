@@ -207,13 +207,17 @@ constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_F
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF>
 __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     k_force(const __grid_constant__ ForceArgs<R> a) {
-  constexpr bool kCache = G <= 8;     // register cache of d zeta / d x_k
-  constexpr int kUnroll = kCache ? G - 1 : 2;   // the trip count: full unroll keeps the cache in registers
-  // FP64, G = 8: early exit at the warp's largest count keeps the loop rolled
-  // and the cache in (L1-backed) local memory, which measured 2-6% faster
-  // than the unrolled, register-capped form; float unrolls (liquid512k /
-  // sic256k sweeps, profiles/r01)
-  constexpr bool kRolled = G == 8 && std::is_same<R, double>::value;
+#ifndef TSF_CACHE_G16
+#define TSF_CACHE_G16 1
+#endif
+  // cache of d zeta / d x_k for the scatter pass (else recomputed there)
+  constexpr bool kCache = G <= 8 || (G == 16 && TSF_CACHE_G16);
+  constexpr int kUnroll = kCache && G <= 8 ? G - 1 : 2;   // full unroll keeps it in registers
+  // FP64 G = 8 and G = 16: early exit at the warp's largest count keeps the
+  // loop rolled and the cache in (L1-backed) local memory — for FP64 G = 8
+  // 2-6% faster than the unrolled, register-capped form; float G = 8 unrolls
+  // (liquid512k / sic256k sweeps, tools/ab.py)
+  constexpr bool kRolled = (G == 8 && std::is_same<R, double>::value) || G == 16;
   constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
   __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
   __shared__ double scut[SPEC == kSingle ? 1 : kRows];
