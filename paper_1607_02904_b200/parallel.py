@@ -88,8 +88,9 @@ class GpuEngine:
     def build(self, cutoff: float, skin: float):
         self.ctx.build_neighbor_list(cutoff, skin)
 
-    def gather_positions(self, idx: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((len(idx), 3), dtype=torch.float64, device=self.device)
+    def gather_positions(self, idx: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((len(idx), 3), dtype=torch.float64, device=self.device)
         if len(idx):
             self.ctx._ok(self._lib.tsf_gather_positions(self.ctx._h, self._p(idx), len(idx),
                                                         self._p(out)))
@@ -103,8 +104,9 @@ class GpuEngine:
         self.ctx.compute(precision, deterministic=deterministic, energy=False, forces=False,
                          virial=False)
 
-    def ghost_forces(self, lo: int, m: int) -> torch.Tensor:
-        out = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+    def ghost_forces(self, lo: int, m: int, out: torch.Tensor = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((m, 3), dtype=torch.float64, device=self.device)
         if m:
             self.ctx._ok(self._lib.tsf_gather_forces(self.ctx._h, lo, m, self._p(out)))
         return out
@@ -204,17 +206,25 @@ class Decomposition:
         self.engine.build(cutoff, skin)
         self.t_send_left = torch.from_numpy(self.send_left.astype(np.int32)).to(dev)
         self.t_send_right = torch.from_numpy(self.send_right.astype(np.int32)).to(dev)
+        # per-step buffers and exchange lists, allocated once per setup (the
+        # step's host work is then a handful of launches and one P2P batch
+        # per direction — it must stay below the GPU time of a step at 8 GPUs)
+        def buf(m):
+            return torch.empty((m, 3), dtype=torch.float64, device=dev)
+        nl, nr = len(self.send_left), len(self.send_right)
+        self._pos_send_l, self._pos_send_r = buf(nl), buf(nr)
+        self._pos_from_l, self._pos_from_r = buf(self.n_gl), buf(self.n_gr)
+        self._f_ghost_l, self._f_ghost_r = buf(self.n_gl), buf(self.n_gr)
+        self._f_to_l, self._f_to_r = buf(nl), buf(nr)
 
     # ---- one force evaluation ------------------------------------------
     def forward(self):
         """Refresh ghost positions from their owners."""
         if self.world == 1:
             return
-        dev = self._device()
-        send_l = self.engine.gather_positions(self.t_send_left)
-        send_r = self.engine.gather_positions(self.t_send_right)
-        from_l = torch.empty((self.n_gl, 3), dtype=torch.float64, device=dev)
-        from_r = torch.empty((self.n_gr, 3), dtype=torch.float64, device=dev)
+        send_l = self.engine.gather_positions(self.t_send_left, out=self._pos_send_l)
+        send_r = self.engine.gather_positions(self.t_send_right, out=self._pos_send_r)
+        from_l, from_r = self._pos_from_l, self._pos_from_r
         self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
                        [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
         self.engine.scatter_positions(self.n_owned, from_l)
@@ -224,11 +234,9 @@ class Decomposition:
         """Send ghost forces home and add them to the owners' forces."""
         if self.world == 1:
             return
-        dev = self._device()
-        f_gl = self.engine.ghost_forces(self.n_owned, self.n_gl)
-        f_gr = self.engine.ghost_forces(self.n_owned + self.n_gl, self.n_gr)
-        to_l = torch.empty((len(self.send_left), 3), dtype=torch.float64, device=dev)
-        to_r = torch.empty((len(self.send_right), 3), dtype=torch.float64, device=dev)
+        f_gl = self.engine.ghost_forces(self.n_owned, self.n_gl, out=self._f_ghost_l)
+        f_gr = self.engine.ghost_forces(self.n_owned + self.n_gl, self.n_gr, out=self._f_ghost_r)
+        to_l, to_r = self._f_to_l, self._f_to_r
         # my right ghosts are the right neighbour's send_left; my left ghosts its send_right
         self._exchange([(f_gr, self.right, TAG_REV_RIGHT), (f_gl, self.left, TAG_REV_LEFT)],
                        [(to_l, self.left, TAG_REV_RIGHT), (to_r, self.right, TAG_REV_LEFT)])

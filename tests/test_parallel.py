@@ -37,8 +37,9 @@ class OracleEngine:
         self.off, self.nb = self.oracle.build_neighbor_list(self.xyz, self.box, self.per, cutoff,
                                                             skin)
 
-    def gather_positions(self, idx):
-        return torch.from_numpy(self.xyz[idx.numpy()].copy())
+    def gather_positions(self, idx, out=None):
+        t = torch.from_numpy(self.xyz[idx.numpy()].copy())
+        return out.copy_(t) if out is not None else t
 
     def scatter_positions(self, lo, t):
         self.xyz[lo:lo + len(t)] = t.numpy()
@@ -49,8 +50,9 @@ class OracleEngine:
         self.f = r["forces"].copy()
         self.ev = np.concatenate([[r["energy"]], r["virial"]])
 
-    def ghost_forces(self, lo, m):
-        return torch.from_numpy(self.f[lo:lo + m].copy())
+    def ghost_forces(self, lo, m, out=None):
+        t = torch.from_numpy(self.f[lo:lo + m].copy())
+        return out.copy_(t) if out is not None else t
 
     def add_forces(self, idx, t):
         self.f[idx.numpy()] += t.numpy()
