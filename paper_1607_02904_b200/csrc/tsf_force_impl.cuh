@@ -654,7 +654,7 @@ Row<R> make_row(const Entry& e) {
   r.m3 = R(e.m == 3 ? 1 : 0);
   r.beta = R(e.beta);
   r.eta = R(e.eta);
-  r.nhie = R(-0.5 / e.eta);
+  r.nhie = R(e.eta > 0 ? -0.5 / e.eta : 0.0);   // eta = 0 only on unused cross rows
   r.big_r = R(e.big_r);
   r.inv2d = R(0.5 / e.big_d);
   r.rmd = R(e.big_r - e.big_d);

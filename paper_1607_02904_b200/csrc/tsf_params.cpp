@@ -61,8 +61,12 @@ double to_number(const Word& w, std::string_view src, const char* field) {
   return v;
 }
 
-// Field constraints of params.cpp:74-92.
-void check_entry(const Entry& e, const std::string& who) {
+// Field constraints of params.cpp:74-92.  One extension (LAMMPS-format
+// files): a cross row (i, j, k) with j != k may carry
+// eta = 0 — LAMMPS SiC-type files write n = beta = 0 there, because the bond
+// order b_ij and the pair terms only ever read the (i, j, j) row
+// (potential.hpp:204-222); rows (i, j, j) keep the reference's eta > 0.
+void check_entry(const Entry& e, const std::string& who, bool cross) {
   const double v[14] = {double(e.m), e.gamma, e.lambda3, e.c, e.d, e.h, e.eta,
                         e.beta, e.lambda2, e.big_b, e.big_r, e.big_d, e.lambda1, e.big_a};
   auto bad = [&](const std::string& why) { throw ParseError("entry " + who + ": " + why); };
@@ -71,7 +75,8 @@ void check_entry(const Entry& e, const std::string& who) {
   if (e.m != 1 && e.m != 3) bad("field 'm' must be 1 or 3");
   if (!(e.big_d > 0)) bad("field 'D' must be positive");
   if (!(e.big_r > e.big_d)) bad("field 'R' must exceed D");
-  if (!(e.eta > 0)) bad("field 'eta' must be positive");
+  if (cross ? !(e.eta >= 0) : !(e.eta > 0))
+    bad(cross ? "field 'eta' must be non-negative" : "field 'eta' must be positive");
   if (e.beta < 0) bad("field 'beta' must be non-negative");
   if (e.d == 0) bad("field 'd' must be nonzero");
   if (e.big_a < 0) bad("field 'A' must be non-negative");
@@ -98,7 +103,7 @@ Params::Params(std::vector<std::string> species, std::vector<Entry> entries)
     for (std::size_t j = 0; j < s; ++j)
       for (std::size_t k = 0; k < s; ++k)
         check_entry(entries_[(i * s + j) * s + k],
-                    species_[i] + " " + species_[j] + " " + species_[k]);
+                    species_[i] + " " + species_[j] + " " + species_[k], j != k);
   for (const Entry& e : entries_) r_cut_max_ = std::max(r_cut_max_, e.cutoff());
 }
 

@@ -108,3 +108,18 @@ def dense_random(tb, n=1200, density=0.14, dmin=1.5, seed=21, skin=0.5):
         m += 1
     return Case(f"dense_random{n}", pts, np.zeros(n, np.int32), box, np.ones(3, np.uint8), skin,
                 si_text(tb))
+
+
+def lammps_style(text):
+    """The same table as LAMMPS writes it: n = beta = 0 on the cross rows
+    (i, j, k), j != k, whose bond-order fields are never read (only (i, j, j)
+    rows feed b_ij and the pair terms)."""
+    out = []
+    for line in text.splitlines():
+        t = line.split()
+        if len(t) == 17 and not line.lstrip().startswith("#") and t[1] != t[2]:
+            t[9] = "0.0"    # eta (n)
+            t[10] = "0.0"   # beta
+            line = " ".join(t)
+        out.append(line)
+    return "\n".join(out) + "\n"

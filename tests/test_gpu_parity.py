@@ -338,3 +338,20 @@ def test_short_export_keeps_reference_filter(tb, oracle, sic_text):
         soff, snb = ctx.export_neighbors("short")
         assert np.array_equal(soff, xoff) and np.array_equal(snb, xnb)
     ctx.close()
+
+
+def test_lammps_style_table_gives_identical_results(tb, sic_text):
+    """n = beta = 0 on the cross rows changes nothing: those fields are never
+    read, so the LAMMPS-format table gives bitwise the same energy, forces and
+    virial as the golden file (which carries n = 1 there)."""
+    case = systems.zincblende(tb, sic_text, 4, jitter=0.1, seed=1, skin=0.5)
+    out = []
+    for text in (case.params_text, systems.lammps_style(case.params_text)):
+        params = tb.parse_params(text)
+        ctx = tb.Context(params, 0)
+        ctx.set_system(case.xyz, case.species, case.box, case.periodic)
+        ctx.build_neighbor_list(params.r_cut_max, case.skin)
+        out.append([ctx.compute(p, deterministic=True) for p in ("double", "mixed", "single")])
+        ctx.close()
+    for (e1, f1, w1), (e2, f2, w2) in zip(*out):
+        assert e1 == e2 and np.array_equal(f1, f2) and np.array_equal(w1, w2)

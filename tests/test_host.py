@@ -52,6 +52,24 @@ def test_sic_table(tb):
     np.testing.assert_array_equal(p.rows, parse_param_text(text).rows)
 
 
+def test_lammps_style_cross_rows(tb):
+    """LAMMPS-format tables (n = beta = 0 on cross rows (i, j, k), j != k,
+    whose bond-order fields are never read) parse; a zero eta on an
+    (i, j, j) row is still refused, as the reference refuses it."""
+    import systems
+    text = open(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")).read()
+    lmp = systems.lammps_style(text)
+    assert lmp != text
+    p, q = tb.parse_params(lmp), tb.parse_params(text)
+    assert p.species_names == q.species_names and p.r_cut_max == q.r_cut_max
+    bad = lmp.replace("C  Si Si 3.0 1.0 0.0 3.8049e4 4.3484 -0.57058 0.72751",
+                      "C  Si Si 3.0 1.0 0.0 3.8049e4 4.3484 -0.57058 0.0")
+    assert bad != lmp
+    with pytest.raises(tb.ParseError) as exc:
+        tb.parse_params(bad)
+    assert "'eta' must be positive" in str(exc.value)
+
+
 @pytest.mark.parametrize("text,needle", [
     ("", "no entries found"),
     ("Si Si Si 1 2 3", "truncated entry"),
