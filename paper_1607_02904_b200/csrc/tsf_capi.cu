@@ -161,6 +161,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.n = n;
     c.sorted = false;
     c.n_owned = -1;
+    ++c.list_version;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
     c.pos.reserve(nn);
@@ -235,23 +236,86 @@ void finish(Ctx& c, double* energy, double* forces, double* virial) {
     for (int q = 0; q < 6; ++q) virial[q] = res[1 + q];
 }
 
+// One evaluation's device work: the short-list filter and the force launches.
+void evaluate_launches(Ctx& c, tsf::Precision p, std::uint32_t flags) {
+  c.mark(0);
+  // The short list is rebuilt from the skin list on every evaluation, as the
+  // reference does (kernels.hpp:187-188).  A filter fused into the force
+  // kernel measured slower (profiles/r01): its gathers then sit
+  // in the register-limited force kernel.  Pairs beyond every cutoff of their
+  // species pair are dropped here as well: they add exact zeros in the
+  // reference (the kernel tests the same exact r^2).
+  tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
+  c.mark(1);
+  tsf::compute(c, p, flags);
+  c.mark(4);
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TSF_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Steady-state evaluations replay a CUDA graph of evaluate_launches: between
+// list rebuilds every launch has the same configuration and arguments (device
+// buffers, group width, grid sizes), so at small N — where ~10 launches and
+// memsets per step, not the GPU, set the pace — one graph launch replaces
+// them.  The key covers everything a launch's arguments depend on; a graph is
+// captured on the second evaluation with a key (the first, eager one grows
+// every buffer), never right after a rebuild (the filter then reads the
+// short-count distribution back synchronously) and never while profiling.
 void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
   if (!c.has_potential)
     throw tsf::ConfigError("context was created without a parameter table (list-only)");
   if (!c.skin_list.valid)
     throw tsf::ConfigError(
         "no neighbor list: call tsf_build_neighbor_list or tsf_set_neighbor_list first");
-  c.mark(0);
-  // The short list is rebuilt from the skin list on every evaluation, as the
-  // reference does (kernels.hpp:187-188).  A filter fused into the force
-  // kernel measured slower at 2M atoms (0.90 vs 0.66 ms, f64, profiles/r01):
-  // its gathers then sit in the low-occupancy FP64 kernel.  Pairs beyond
-  // every cutoff of their species pair are dropped here as well: they add
-  // exact zeros in the reference (the kernel tests the same exact r^2).
-  tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
-  c.mark(1);
-  tsf::compute(c, p, flags);
-  c.mark(4);
+  const int mode = int((flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
+  const bool steady = !c.short_max_stale && c.short_apply == mode;
+  const std::uint64_t key[6] = {c.list_version, std::uint64_t(p), flags, std::uint64_t(c.n),
+                                std::uint64_t(c.n_owned),
+                                std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
+  const bool graphable = graphs_enabled() && !c.graphs_off && !c.profile && steady && c.n > 0;
+  if (graphable && c.graph_exec && std::equal(key, key + 6, c.graph_key)) {
+    TSF_CUDA(cudaGraphLaunch(c.graph_exec, c.stream));
+    c.launches += c.graph_launches;
+  } else if (graphable && std::equal(key, key + 6, c.warm_key)) {
+    if (c.graph_exec) {
+      TSF_CUDA(cudaGraphExecDestroy(c.graph_exec));
+      c.graph_exec = nullptr;
+    }
+    const std::int64_t l0 = c.launches;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        evaluate_launches(c, p, flags);
+      } catch (...) {
+        ok = false;
+      }
+      ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
+      ok = ok && cudaGraphInstantiate(&c.graph_exec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    if (ok) {
+      c.graph_launches = c.launches - l0;
+      std::copy(key, key + 6, c.graph_key);
+      TSF_CUDA(cudaGraphLaunch(c.graph_exec, c.stream));
+    } else {   // capture refused: clear the sticky error and stay eager
+      cudaGetLastError();
+      if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
+      c.graph_exec = nullptr;
+      c.graphs_off = true;
+      c.launches = l0;
+      evaluate_launches(c, p, flags);
+    }
+  } else {
+    evaluate_launches(c, p, flags);
+    std::copy(key, key + 6, c.warm_key);
+  }
   c.forces_current = true;
   if (c.profile) {
     TSF_CUDA(cudaEventSynchronize(c.ev[4]));
@@ -404,6 +468,7 @@ void tsf_destroy(tsf_ctx* ctx) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.pinned) cudaFreeHost(c.pinned);
   c.pinned = nullptr;
+  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
   for (auto& e : c.ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = c.own_stream;       // never destroy a caller's stream
@@ -423,6 +488,7 @@ int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned) {
   return guard(&ctx->c, [&] {
     if (n_owned > ctx->c.n) throw tsf::ConfigError("owned count exceeds the atom count");
     ctx->c.n_owned = n_owned < 0 ? -1 : n_owned;
+    ++ctx->c.list_version;
     ctx->c.forces_current = false;
   });
 }
@@ -551,6 +617,7 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
     c.cutoff = cutoff;
     c.skin = skin;
     c.short_max_stale = true;
+    ++c.list_version;
     tsf::snapshot_reference_positions(c);
   });
 }

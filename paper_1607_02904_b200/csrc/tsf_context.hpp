@@ -110,6 +110,15 @@ struct Ctx {
                                // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
   DevBuf<int> overflow;        // [2n] tier queues: atoms over the group width / over 16
 
+  // CUDA graph of the steady-state evaluation (filter + force launches),
+  // replayed while its key holds; see evaluate() in tsf_capi.cu
+  std::uint64_t list_version = 0;      // bumped by every list / centre-set change
+  cudaGraphExec_t graph_exec = nullptr;
+  std::uint64_t graph_key[6] = {};     // key of graph_exec
+  std::uint64_t warm_key[6] = {};      // key of the last eager evaluation
+  std::int64_t graph_launches = 0;     // kernels per replay
+  bool graphs_off = false;             // capture failed once: stay eager
+
   // MD state
   DevBuf<double> vel;          // [n][3]
   std::vector<double> masses;  // per species

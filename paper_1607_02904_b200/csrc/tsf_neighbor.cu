@@ -545,6 +545,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
   snapshot_reference_positions(c);
   c.short_max_stale = true;
   c.short_list.valid = false;
+  ++c.list_version;
 }
 
 void snapshot_reference_positions(Ctx& c) {

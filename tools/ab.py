@@ -1,7 +1,8 @@
 """A/B two builds of the library on the same GPU box: alternate
 `TSF_LIBRARY=<a>` / `<b>` bench runs (device-resident, all precisions as
 variants) R times and print the median kernel and step times per config.
-usage: python tools/ab.py <lib_a> <lib_b> [rounds] [config...]"""
+usage: python tools/ab.py <lib_a> <lib_b> [rounds] [config...]
+(a "lib" may also be "+NAME=VALUE": the default library with that env setting)"""
 import json
 import os
 import statistics
@@ -12,7 +13,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(lib, cfg):
-    env = dict(os.environ, TSF_LIBRARY=lib) if lib else dict(os.environ)
+    # lib: a library path, or "+NAME=VALUE" (the default library with an env setting)
+    if lib.startswith("+"):
+        k, v = lib[1:].split("=", 1)
+        env = dict(os.environ, **{k: v})
+    else:
+        env = dict(os.environ, TSF_LIBRARY=lib) if lib else dict(os.environ)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg,
                           "--steps", "300", "--no-cpu-baseline", "--no-e2e"],
                          capture_output=True, text=True, env=env, timeout=600)
