@@ -103,12 +103,13 @@ struct Ctx {
   DevBuf<double> atom_ev;      // deterministic tier launches: [n][8] energy + virial
   DevBuf<double> partials;     // [blocks][kRedWidth]
   DevBuf<double> result;       // energy + virial (7), reduced
-  DevBuf<int> flags;           // [0] error bits, [1]/[2] tier queue counts (force path;
-                               // [2] doubles as the rebuild flag, read synchronously),
+  DevBuf<int> flags;           // [0] error bits, [1..3] tier queue counts (force path;
+                               // [2] doubles as the rebuild flag and [3] as the largest
+                               // skin count, both read synchronously in their own calls),
                                // [3] largest skin count, [4] largest short count,
                                // [5] |coord| max bits, [6] max cell occupancy,
                                // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
-  DevBuf<int> overflow;        // [2n] tier queues: atoms over the group width / over 16
+  DevBuf<int> overflow;        // [3n] tier queues (G = 8, 16, 32 inputs)
 
   // CUDA graph of the steady-state evaluation (filter + force launches),
   // replayed while its key holds; see evaluate() in tsf_capi.cu

@@ -730,11 +730,17 @@ void run_force(Ctx& c, ForceArgs<R> a) {
   const char* pin = std::getenv("TSF_GROUP_WIDTH");
   const int pinned = pin ? std::atoi(pin) : 0;
   if (pinned == 4 || pinned == 8 || pinned == 16 || pinned == 32) g = pinned;
-  // queues: [0, n) atoms over the main width, [n, 2n) atoms over 16;
-  // counts in flags[1] / flags[2] (zeroed with the error bits per evaluation)
-  int* q1 = c.overflow.get();
-  int* q2 = q1 + c.n;
-  a.ovf_out = g < 32 ? q1 : nullptr;
+  // Tier chain: atoms over the main width are queued for G = 8 (when the
+  // last rebuild saw counts over 4), then G = 16 (counts over 8), then
+  // G = 32, which takes whatever is left — including atoms that outgrew the
+  // width since the rebuild (an idle tier launch still costs ~3 us).  At
+  // 1600 K a few % of Si atoms gain a 5th neighbour: the G = 8 tier takes
+  // them at 4 atoms per warp instead of G = 16's 2.  Queue q holds
+  // [q n, (q + 1) n) of c.overflow; its count is flags[1 + q] (zeroed with
+  // the error bits per evaluation).
+  int* qbuf = c.overflow.get();
+  int cur = 0;                              // queue the main launch fills
+  a.ovf_out = g < 32 ? qbuf : nullptr;
   a.ovf_out_count = a.flags + 1;
   int nb = 0;
   switch (g) {
@@ -743,29 +749,22 @@ void run_force(Ctx& c, ForceArgs<R> a) {
     case 16: nb = launch_main<R, Acc, 16, SPEC, DET>(c, a); break;
     default: nb = launch_main<R, Acc, 32, SPEC, DET>(c, a); break;
   }
-  // The G=16 tier runs only when atoms were over the width at the last
-  // rebuild; otherwise the queue holds the few that outgrew it since, and
-  // the G=32 tier alone takes them (an idle launch still costs ~3 us).
-  const bool tier16 = g < 16 && mx > g;
-  if (tier16) {
+  auto tier = [&](auto kernel, int blocks, bool last) {
     a.partial_base = nb;
-    a.ovf_in = q1;
-    a.ovf_in_count = a.flags + 1;
-    a.ovf_out = q2;
-    a.ovf_out_count = a.flags + 2;
-    k_force<R, Acc, 16, SPEC, DET, true><<<kOverflowBlocks, kBlock, 0, c.stream>>>(a);
-    nb += kOverflowBlocks;
+    a.ovf_in = qbuf + std::size_t(cur) * c.n;
+    a.ovf_in_count = a.flags + 1 + cur;
+    a.ovf_out = last ? nullptr : qbuf + std::size_t(cur + 1) * c.n;
+    a.ovf_out_count = a.flags + 2 + cur;
+    kernel<<<blocks, kBlock, 0, c.stream>>>(a);
+    nb += blocks;
     ++c.launches;
-  }
+    if (!last) ++cur;
+  };
+  if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true>, kOverflowBlocks, false);
+  if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true>, kOverflowBlocks, false);
   if (g < 32) {
-    a.partial_base = nb;
-    a.ovf_in = tier16 ? q2 : q1;
-    a.ovf_in_count = a.flags + (tier16 ? 2 : 1);
-    a.ovf_out = nullptr;
-    const int blocks32 = g == 16 ? kOverflowBlocks : kOverflowBlocks / 4;
-    k_force<R, Acc, 32, SPEC, DET, true><<<blocks32, kBlock, 0, c.stream>>>(a);
-    nb += blocks32;
-    ++c.launches;
+    tier(k_force<R, Acc, 32, SPEC, DET, true>, mx > 16 ? kOverflowBlocks : kOverflowBlocks / 4,
+         true);
     if (DET) {
       k_queued_ev<<<kOverflowBlocks, kBlock, 0, c.stream>>>(
           a.atom_ev, a.cnt, a.perm, a.n_owned, a.center_limit, g, a.flags + 1,
@@ -808,10 +807,10 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.cutsq = c.cutsq.get();
   a.ns = c.params.species_count();
   a.flags = c.flags.get();
-  c.overflow.reserve(std::max<std::size_t>(2 * n, 1));
-  c.partials.reserve(std::size_t(32 * 148 + 3 * kOverflowBlocks + 8) * kRedWidth);
+  c.overflow.reserve(std::max<std::size_t>(3 * n, 1));
+  c.partials.reserve(std::size_t(32 * 148 + 4 * kOverflowBlocks + 8) * kRedWidth);
   a.partials = c.partials.get();
-  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 3 * sizeof(int), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));
 
   constexpr bool kF32 = std::is_same<Acc, float>::value;
   if (det) {
