@@ -766,15 +766,24 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
     };
     if (!c.forces_current) evaluate(c, p, flags);
     sample(0);
+    // velocity Verlet (engine.cpp:142-172).  The closing half-kick of a step
+    // is deferred into the next step's opening kick + drift (one pass over
+    // the atoms instead of two) unless a sample needs full-step velocities.
+    bool kick_pending = false;
     for (std::int64_t s = 1; s <= steps; ++s) {
-      tsf::md_kick(c, dt, true);
+      tsf::md_kick(c, dt, true, kick_pending ? 2 : 1);
       if (tsf::list_needs_rebuild(c)) {
         tsf::list_build(c, c.cutoff, c.skin);
         ++nreb;
       }
       evaluate(c, p, flags);
-      tsf::md_kick(c, dt, false);
-      if (s % thermo_every == 0 || s == steps) sample(s);
+      if (s % thermo_every == 0 || s == steps) {
+        tsf::md_kick(c, dt, false);
+        sample(s);
+        kick_pending = false;
+      } else {
+        kick_pending = true;
+      }
     }
     if (nsamples) *nsamples = ns;
     if (rebuilds) *rebuilds = nreb;

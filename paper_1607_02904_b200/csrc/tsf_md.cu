@@ -133,14 +133,23 @@ struct Masses {
 
 __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n, Masses ms,
-                       double dt, int drift, Box box) {
+                       double dt, int drift, int kicks, Box box) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   double4 p = pos[a];
   const double k = __ddiv_rn(__dmul_rn(0.5, dt), __dmul_rn(ms.m[species_of(p)], kMvv2e));
-  const double vx = __dadd_rn(vel[3 * a], __dmul_rn(f[3 * a], k));
-  const double vy = __dadd_rn(vel[3 * a + 1], __dmul_rn(f[3 * a + 1], k));
-  const double vz = __dadd_rn(vel[3 * a + 2], __dmul_rn(f[3 * a + 2], k));
+  // kicks = 2: the closing half-kick of step s and the opening one of s+1
+  // (same forces, no sample between them) in one pass — the same two
+  // roundings as two launches, so the trajectory is bitwise unchanged
+  const double fx = f[3 * a], fy = f[3 * a + 1], fz = f[3 * a + 2];
+  double vx = __dadd_rn(vel[3 * a], __dmul_rn(fx, k));
+  double vy = __dadd_rn(vel[3 * a + 1], __dmul_rn(fy, k));
+  double vz = __dadd_rn(vel[3 * a + 2], __dmul_rn(fz, k));
+  if (kicks == 2) {
+    vx = __dadd_rn(vx, __dmul_rn(fx, k));
+    vy = __dadd_rn(vy, __dmul_rn(fy, k));
+    vz = __dadd_rn(vz, __dmul_rn(fz, k));
+  }
   vel[3 * a] = vx;
   vel[3 * a + 1] = vy;
   vel[3 * a + 2] = vz;
@@ -330,12 +339,12 @@ void unsort(Ctx& c) {
   refresh_shadow(c);
 }
 
-void md_kick(Ctx& c, double dt, bool drift) {
+void md_kick(Ctx& c, double dt, bool drift, int kicks) {
   if (c.n == 0) return;
   k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), c.posf.get(),
                                                    c.flags.get() + 5, c.vel.get(),
                                                    c.forces.get(), int(c.n), masses_of(c), dt,
-                                                   drift ? 1 : 0, c.box);
+                                                   drift ? 1 : 0, kicks, c.box);
   ++c.launches;
 }
 
