@@ -771,8 +771,13 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
     // the atoms instead of two) unless a sample needs full-step velocities.
     bool kick_pending = false;
     for (std::int64_t s = 1; s <= steps; ++s) {
-      tsf::md_kick(c, dt, true, kick_pending ? 2 : 1);
-      if (tsf::list_needs_rebuild(c)) {
+      // kick + drift + the rebuild test in one pass; only its flag comes back
+      tsf::md_kick(c, dt, true, kick_pending ? 2 : 1, /*check_rebuild=*/true);
+      int moved = 0;
+      TSF_CUDA(cudaMemcpyAsync(&moved, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                               c.stream));
+      TSF_CUDA(cudaStreamSynchronize(c.stream));
+      if (moved) {
         tsf::list_build(c, c.cutoff, c.skin);
         ++nreb;
       }

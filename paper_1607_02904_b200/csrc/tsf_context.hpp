@@ -174,8 +174,9 @@ void add_forces(Ctx& c, const int* d_idx, std::int64_t m, const double* d_f);
 void refresh_shadow(Ctx& c);           // posf = float(pos)
 void pack_velocities(Ctx& c);          // xyz_stage (user order velocities) -> vel (slots)
 void unpack_velocities(Ctx& c);        // vel (slots) -> xyz_stage (user order)
-// v += F dt/(2 m mvv2e), `kicks` (1 or 2) times in a row [; x += v dt, wrap]
-void md_kick(Ctx& c, double dt, bool drift, int kicks = 1);
+// v += F dt/(2 m mvv2e), `kicks` (1 or 2) times in a row [; x += v dt, wrap
+// [; the needs_rebuild test on the new positions -> flags[2]]]
+void md_kick(Ctx& c, double dt, bool drift, int kicks = 1, bool check_rebuild = false);
 void md_kinetic(Ctx& c);               // KE -> result[7] (device)
 void md_scale_velocities(Ctx& c, double factor);
 

@@ -133,7 +133,9 @@ struct Masses {
 
 __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n, Masses ms,
-                       double dt, int drift, int kicks, Box box) {
+                       double dt, int drift, int kicks, Box box,
+                       const double4* __restrict__ ref, double limit_sq,
+                       int* __restrict__ moved_flag) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   double4 p = pos[a];
@@ -163,6 +165,13 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
     pos[a] = p;
     posf[a] = shadow(p);
     track_coord_max(cmax, p);
+    if (moved_flag) {   // needs_rebuild (neighbor.cpp:134-141) on the new position
+      double dx, dy, dz;
+      displacement(ref[a], p, box, dx, dy, dz);
+      const bool moved = norm_sq_exact(dx, dy, dz) > limit_sq;
+      const unsigned act = __activemask();
+      if (__any_sync(act, moved) && (threadIdx.x & 31) == __ffs(act) - 1) atomicOr(moved_flag, 1);
+    }
   }
 }
 
@@ -339,12 +348,14 @@ void unsort(Ctx& c) {
   refresh_shadow(c);
 }
 
-void md_kick(Ctx& c, double dt, bool drift, int kicks) {
+void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
   if (c.n == 0) return;
-  k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), c.posf.get(),
-                                                   c.flags.get() + 5, c.vel.get(),
-                                                   c.forces.get(), int(c.n), masses_of(c), dt,
-                                                   drift ? 1 : 0, kicks, c.box);
+  const bool check = drift && check_rebuild;
+  if (check) TSF_CUDA(cudaMemsetAsync(c.flags.get() + 2, 0, sizeof(int), c.stream));
+  k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+      c.pos.get(), c.posf.get(), c.flags.get() + 5, c.vel.get(), c.forces.get(), int(c.n),
+      masses_of(c), dt, drift ? 1 : 0, kicks, c.box, c.pos_ref.get(), 0.25 * c.skin * c.skin,
+      check ? c.flags.get() + 2 : nullptr);
   ++c.launches;
 }
 
