@@ -141,7 +141,9 @@ int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset);
  * they own); forces land on owned and ghost atoms alike and the caller sends
  * the ghost part back to the owners.  Pointers marked d_ are device pointers
  * on the context's device; all work is ordered on the context's stream. */
-int tsf_set_stream(tsf_ctx* ctx, void* stream);   /* NULL: back to the context's own */
+/* NULL: back to the context's own (non-blocking) stream — pass a real
+ * stream, not the legacy default stream's 0, to share ordering with a caller */
+int tsf_set_stream(tsf_ctx* ctx, void* stream);
 int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned);  /* default: all atoms */
 /* d_xyz[m][3] = positions of user atoms d_idx[0..m) */
 int tsf_gather_positions(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, double* d_xyz);
@@ -166,6 +168,15 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
 /* v *= factor for every atom (velocity-rescaling thermostat for fixture
  * generation, e.g. the liquid-Si melt of SURVEY.md 8d cfg 5). */
 int tsf_md_scale_velocities(tsf_ctx* ctx, double factor);
+/* One velocity-Verlet piece for drivers that interleave communication (the
+ * slab decomposition's distributed NVE): v += F dt/(2 m mvv2e), `kicks` (1
+ * or 2) times in a row, then with drift != 0 x += v dt, wrap, and the
+ * needs_rebuild test (neighbor.cpp:134-141) on the new positions, whose
+ * result goes to *moved when moved != NULL (engine.cpp:142-172).  Owned atoms
+ * only (tsf_set_owned); ghosts are refreshed by the exchange. */
+int tsf_md_kick(tsf_ctx* ctx, double dt, int drift, int kicks, int* moved);
+/* Kinetic energy of the owned atoms, eV (system.cpp:16-21). */
+int tsf_md_kinetic(tsf_ctx* ctx, double* ke);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,8 @@ PROTOTYPES = [
     ("tsf_add_forces", C.c_int, [_vp, _vp, C.c_int64, _vp]),
     ("tsf_results_device", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_scale_velocities", C.c_int, [_vp, C.c_double]),
+    ("tsf_md_kick", C.c_int, [_vp, _d, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    ("tsf_md_kinetic", C.c_int, [_vp, _dptr]),
     ("tsf_md_set_state", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_get_state", C.c_int, [_vp, _vp, _vp]),
     ("tsf_md_run", C.c_int, [_vp, C.c_int, C.c_int64, _d, C.c_uint32, C.c_int, _vp, C.c_int64,

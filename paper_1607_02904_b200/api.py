@@ -388,6 +388,21 @@ class Context:
     def md_scale_velocities(self, factor: float):
         self._ok(self._lib.tsf_md_scale_velocities(self._h, float(factor)))
 
+    def md_kick(self, dt: float, drift: bool = True, kicks: int = 1, check: bool = True):
+        """One velocity-Verlet piece (tsf_md_kick): `kicks` half-kicks, then
+        with drift the position update, wrap and the rebuild test; returns
+        whether some owned atom moved more than skin/2 since the list build."""
+        moved = C.c_int(0)
+        self._ok(self._lib.tsf_md_kick(self._h, float(dt), int(bool(drift)), int(kicks),
+                                       C.byref(moved) if check else None))
+        return bool(moved.value)
+
+    def md_kinetic(self) -> float:
+        """Kinetic energy of the owned atoms, eV."""
+        ke = C.c_double(0.0)
+        self._ok(self._lib.tsf_md_kinetic(self._h, C.byref(ke)))
+        return ke.value
+
     def md_get_state(self):
         x = np.zeros((self.n, 3))
         v = np.zeros((self.n, 3))

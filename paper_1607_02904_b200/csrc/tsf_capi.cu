@@ -738,6 +738,41 @@ int tsf_md_scale_velocities(tsf_ctx* ctx, double factor) {
   });
 }
 
+int tsf_md_kick(tsf_ctx* ctx, double dt, int drift, int kicks, int* moved) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (!(dt > 0.0)) throw tsf::ConfigError("dt must be positive");
+    if (kicks != 1 && kicks != 2) throw tsf::ConfigError("kicks must be 1 or 2");
+    if (c.masses.empty()) throw tsf::ConfigError("call tsf_md_set_state before tsf_md_kick");
+    const bool check = drift && moved && c.skin_list.valid;
+    tsf::md_kick(c, dt, drift != 0, kicks, check);
+    if (drift) c.forces_current = false;
+    if (moved) {
+      int f = 0;
+      if (check)
+        TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                                 c.stream));
+      TSF_CUDA(cudaStreamSynchronize(c.stream));
+      *moved = check ? f : 1;   // no list: a build is due anyway
+    }
+  });
+}
+
+int tsf_md_kinetic(tsf_ctx* ctx, double* ke) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (c.masses.empty()) throw tsf::ConfigError("call tsf_md_set_state before tsf_md_kinetic");
+    double v = 0.0;
+    if (c.n > 0) {
+      tsf::md_kinetic(c);
+      TSF_CUDA(cudaMemcpyAsync(&v, c.result.get() + 7, sizeof(double), cudaMemcpyDeviceToHost,
+                               c.stream));
+      TSF_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    *ke = v;
+  });
+}
+
 int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t flags,
                int thermo_every, double* thermo, int64_t cap, int64_t* nsamples,
                int64_t* rebuilds) {

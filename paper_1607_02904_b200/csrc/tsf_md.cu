@@ -135,9 +135,13 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n, Masses ms,
                        double dt, int drift, int kicks, Box box,
                        const double4* __restrict__ ref, double limit_sq,
-                       int* __restrict__ moved_flag) {
+                       int* __restrict__ moved_flag, const int* __restrict__ perm,
+                       int center_limit) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
+  // a decomposition's ghost copies are integrated by their owners and
+  // refreshed by the forward exchange (center_limit < n only then)
+  if (center_limit < n && (perm ? perm[a] : a) >= center_limit) return;
   double4 p = pos[a];
   const double k = __ddiv_rn(__dmul_rn(0.5, dt), __dmul_rn(ms.m[species_of(p)], kMvv2e));
   // kicks = 2: the closing half-kick of step s and the opening one of s+1
@@ -179,10 +183,13 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
 // fixed order then one block finishing the sum: deterministic.
 __global__ void __launch_bounds__(256) k_ke_partial(const double4* __restrict__ pos,
                                                     const double* __restrict__ vel, int n,
-                                                    Masses ms, double* __restrict__ part) {
+                                                    Masses ms, double* __restrict__ part,
+                                                    const int* __restrict__ perm,
+                                                    int center_limit) {
   __shared__ double s[256];
   double acc = 0;
   for (int a = blockIdx.x * 256 + threadIdx.x; a < n; a += gridDim.x * 256) {
+    if (center_limit < n && (perm ? perm[a] : a) >= center_limit) continue;   // ghosts
     const double m = ms.m[species_of(pos[a])];
     const double vx = vel[3 * a], vy = vel[3 * a + 1], vz = vel[3 * a + 2];
     acc += 0.5 * m * (vx * vx + vy * vy + vz * vz) * kMvv2e;
@@ -348,6 +355,10 @@ void unsort(Ctx& c) {
   refresh_shadow(c);
 }
 
+int center_limit(const Ctx& c) {   // user atoms below it are owned (all unless decomposed)
+  return int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
+}
+
 void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
   if (c.n == 0) return;
   const bool check = drift && check_rebuild;
@@ -355,7 +366,7 @@ void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
   k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
       c.pos.get(), c.posf.get(), c.flags.get() + 5, c.vel.get(), c.forces.get(), int(c.n),
       masses_of(c), dt, drift ? 1 : 0, kicks, c.box, c.pos_ref.get(), 0.25 * c.skin * c.skin,
-      check ? c.flags.get() + 2 : nullptr);
+      check ? c.flags.get() + 2 : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c));
   ++c.launches;
 }
 
@@ -363,7 +374,8 @@ void md_kinetic(Ctx& c) {
   constexpr int kParts = 296;
   c.partials.reserve(std::size_t(kParts) * kRedWidth);
   k_ke_partial<<<kParts, 256, 0, c.stream>>>(c.pos.get(), c.vel.get(), int(c.n), masses_of(c),
-                                             c.partials.get());
+                                             c.partials.get(), c.sorted ? c.perm.get() : nullptr,
+                                             center_limit(c));
   k_ke_final<<<1, 256, 0, c.stream>>>(c.partials.get(), kParts, c.result.get() + 7);
   c.launches += 2;
 }

@@ -75,8 +75,17 @@ class GpuEngine:
         self.ctx = Context(params, device)
         self.device = torch.device("cuda", device)
         self._lib = L.lib()
-        self.ctx._ok(self._lib.tsf_set_stream(self.ctx._h,
-                                              C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+        # One stream orders torch's work (allocations, NCCL P2P, .item()) and
+        # the C-ABI's kernels.  torch's legacy default stream has the handle 0,
+        # which tsf_set_stream reads as "the context's own stream" — a
+        # non-blocking stream that does NOT order against it — so the engine
+        # then makes a dedicated stream torch's current one.
+        stream = torch.cuda.current_stream(device)
+        if stream.cuda_stream == 0:
+            stream = torch.cuda.Stream(device)
+            torch.cuda.set_stream(stream)
+        self.stream = stream
+        self.ctx._ok(self._lib.tsf_set_stream(self.ctx._h, C.c_void_p(stream.cuda_stream)))
 
     def _p(self, t: torch.Tensor):
         return C.c_void_p(t.data_ptr())
@@ -121,6 +130,20 @@ class GpuEngine:
         self.ctx._ok(self._lib.tsf_results_device(self.ctx._h, self._p(ev), self._p(f)))
         return ev, f
 
+    # ---- velocity Verlet pieces (SlabNVE) ----
+    def md_set_state(self, velocities: np.ndarray, masses):
+        self.ctx.md_set_state(velocities, masses)
+
+    def md_get_state(self):
+        """Local positions and velocities, user order (owned atoms first)."""
+        return self.ctx.md_get_state()
+
+    def kick(self, dt: float, drift: bool = True, kicks: int = 1) -> bool:
+        return self.ctx.md_kick(dt, drift, kicks, check=drift)
+
+    def kinetic(self) -> float:
+        return self.ctx.md_kinetic()
+
 
 class Decomposition:
     """One rank's view: owned atoms (global ids), ghost blocks, send lists."""
@@ -141,6 +164,7 @@ class Decomposition:
         self.slab = Slab(self.rank, self.world, float(self.box[0]), float(halo))
         self.left = (self.rank - 1) % self.world
         self.right = (self.rank + 1) % self.world
+        self.migrated = 0      # atoms received from neighbours by migrate()
 
     # ---- exchange helpers ------------------------------------------------
     def _device(self):
@@ -248,6 +272,44 @@ class Decomposition:
         self.engine.compute(precision, deterministic)
         self.reverse()
 
+    # ---- atom migration at a rebuild ----------------------
+    def migrate(self, xyz: np.ndarray, vel: np.ndarray, cutoff: float, skin: float):
+        """Owned atoms that left the slab go to the neighbour that owns them
+        now (with species and velocity), arrivals join; ghosts are re-selected
+        and the lists rebuilt (setup).  xyz / vel: this rank's owned atoms in
+        the order of self.gid.  Returns the new owned velocities (self.gid
+        order)."""
+        species = self.local_species[: self.n_owned]
+        if self.world == 1:
+            self.setup(self.gid, xyz, species, cutoff, skin)
+            return np.asarray(vel, np.float64)
+        owner = self.slab.owner(xyz[:, 0])
+        to_l = owner == self.left
+        to_r = (owner == self.right) & ~to_l
+        stay = owner == self.rank
+        if not np.all(stay | to_l | to_r):
+            raise ConfigError("an atom moved farther than one slab between list builds")
+        dev = self._device()
+
+        def pack(m):
+            return torch.from_numpy(np.column_stack([
+                self.gid[m].astype(np.float64), species[m].astype(np.float64), xyz[m],
+                vel[m]])).to(dev)
+        n_l, n_r = self._swap_counts(int(to_l.sum()), int(to_r.sum()))
+        from_l = torch.zeros((n_l, 8), dtype=torch.float64, device=dev)
+        from_r = torch.zeros((n_r, 8), dtype=torch.float64, device=dev)
+        self._exchange([(pack(to_l), self.left, TAG_FWD_LEFT), (pack(to_r), self.right, TAG_FWD_RIGHT)],
+                       [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+        arr = torch.cat([from_l, from_r]).cpu().numpy()
+        self.migrated += len(arr)
+        gid = np.concatenate([self.gid[stay], arr[:, 0].astype(np.int64)])
+        sp = np.concatenate([species[stay], arr[:, 1].astype(np.int32)])
+        x = np.concatenate([xyz[stay], arr[:, 2:5]])
+        v = np.concatenate([vel[stay], arr[:, 5:8]])
+        order = np.argsort(gid, kind="stable")
+        self.setup(gid[order], x[order], sp[order], cutoff, skin)
+        return v[order]
+
     def gather_results(self, total_atoms: int):
         """Energy/virial summed over ranks and global-order forces on rank 0
         (a check/report path, not the per-step loop)."""
@@ -263,6 +325,74 @@ class Decomposition:
             forces[gid] = fo
         e = ev.cpu().numpy()
         return float(e[0]), forces, e[1:7].copy()
+
+
+class SlabNVE:
+    """Velocity-Verlet NVE across the slab decomposition — the MD step of
+    SURVEY.md 8d/8e: every rank integrates its owned atoms (tsf_md_kick),
+    ghosts follow by the forward exchange, forces come back by the reverse
+    exchange, the rebuild decision is the OR over ranks of the reference's
+    needs_rebuild test, and at a rebuild atoms migrate to their new owners
+    before ghosts and lists are rebuilt.  Thermo (potential, kinetic energy)
+    is summed over ranks.  The closing half-kick of a step is deferred into
+    the next opening kick when no sample intervenes, as in tsf_md_run."""
+
+    def __init__(self, dec: "Decomposition", masses, cutoff: float, skin: float,
+                 precision: str = "double", deterministic: bool = False):
+        self.dec = dec
+        self.masses = np.asarray(masses, np.float64)
+        self.cutoff, self.skin = float(cutoff), float(skin)
+        self.precision, self.deterministic = precision, deterministic
+        self.rebuilds = 0
+        self._evaluated = False
+
+    def set_velocities(self, vel_owned: np.ndarray):
+        """Velocities of the owned atoms, in the order of dec.gid."""
+        eng = self.dec.engine
+        v = np.zeros((self.dec.n_owned + len(self.dec.ghost_gid), 3))
+        v[: self.dec.n_owned] = vel_owned
+        eng.md_set_state(v, self.masses)
+
+    def _allreduce(self, values):
+        t = torch.tensor(values, dtype=torch.float64, device=self.dec._device())
+        if self.dec.world > 1:
+            dist.all_reduce(t, group=self.dec.group)
+        return t.cpu().numpy()
+
+    def _sample(self, step):
+        ev, _ = self.dec.engine.results()
+        pe, ke = self._allreduce([float(ev[0].item()), self.dec.engine.kinetic()])
+        return (step, float(pe), float(ke))
+
+    def run(self, steps: int, dt: float = 0.001, thermo_every: int = 100):
+        dec, eng = self.dec, self.dec.engine
+        if not self._evaluated:
+            dec.evaluate(self.precision, self.deterministic)
+            self._evaluated = True
+        samples = [self._sample(0)]
+        pending = False
+        for s in range(1, steps + 1):
+            moved = eng.kick(dt, drift=True, kicks=2 if pending else 1)
+            if self._allreduce([1.0 if moved else 0.0])[0] > 0:
+                x, v = eng.md_get_state()
+                n = dec.n_owned
+                vel = dec.migrate(x[:n], v[:n], self.cutoff, self.skin)
+                self.set_velocities(vel)
+                self.rebuilds += 1
+            dec.evaluate(self.precision, self.deterministic)
+            if s % thermo_every == 0 or s == steps:
+                eng.kick(dt, drift=False)
+                samples.append(self._sample(s))
+                pending = False
+            else:
+                pending = True
+        return samples
+
+    def owned_state(self):
+        """(gid, positions, velocities) of this rank's owned atoms."""
+        x, v = self.dec.engine.md_get_state()
+        n = self.dec.n_owned
+        return self.dec.gid.copy(), x[:n].copy(), v[:n].copy()
 
 
 def partition(xyz: np.ndarray, box, world: int, rank: int, halo: float) -> np.ndarray:

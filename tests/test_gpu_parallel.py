@@ -146,3 +146,36 @@ def test_two_emulated_ranks_match_one_context(tb):
     assert abs(e - e1) <= 1e-12 * abs(e1)
     assert np.abs(f - f1).max() <= 1e-10
     assert np.abs(w - w1).max() <= 1e-10 * np.abs(w1).max()
+
+
+def test_slab_nve_single_rank_matches_md_run(tb):
+    """SlabNVE on one rank (GpuEngine: tsf_md_kick per piece, rebuilds through
+    Decomposition.migrate/setup) reproduces the fused GPU-resident loop
+    tsf_md_run step for step in deterministic mode: same rebuild schedule,
+    same thermo samples, same final state."""
+    from paper_1607_02904_b200.parallel import Decomposition, GpuEngine, SlabNVE
+    params = tb.builtin_silicon()
+    s = tb.make_diamond_lattice(4, 4, 4)
+    tb.init_velocities(s, 1600.0, 12345)
+    skin, steps = 1.0, 60
+    ctx = tb.Context(params, 0)
+    ctx.load(s)
+    ctx.build_neighbor_list(params.r_cut_max, skin)
+    ctx.md_set_state(s.velocities, s.species_masses)
+    thermo, nreb = ctx.md_run(steps, 0.001, "double", deterministic=True, thermo_every=10)
+    x_ref, v_ref = ctx.md_get_state()
+    ctx.close()
+
+    eng = GpuEngine(params, 0)
+    dec = Decomposition(eng, s.box.lengths, s.box.periodic, params.r_cut_max + skin)
+    dec.setup(np.arange(s.natoms), s.positions, s.species, params.r_cut_max, skin)
+    nve = SlabNVE(dec, s.species_masses, params.r_cut_max, skin, deterministic=True)
+    nve.set_velocities(s.velocities)
+    samples = np.array(nve.run(steps, 0.001, thermo_every=10))
+    _, x, v = nve.owned_state()
+    assert nreb >= 1 and nve.rebuilds == nreb
+    np.testing.assert_allclose(samples, thermo, rtol=1e-12, atol=1e-10)
+    dx = x - x_ref
+    dx -= s.box.lengths * np.round(dx / s.box.lengths)
+    assert np.abs(dx).max() < 1e-10
+    assert np.abs(v - v_ref).max() < 1e-8

@@ -36,6 +36,52 @@ class OracleEngine:
     def build(self, cutoff, skin):
         self.off, self.nb = self.oracle.build_neighbor_list(self.xyz, self.box, self.per, cutoff,
                                                             skin)
+        self.skin, self.ref = skin, self.xyz.copy()
+
+    # velocity Verlet pieces with tsf_md_kick's arithmetic (k_kick, tsf_md.cu):
+    # separate roundings, wrap_1d (box.hpp:41-46), needs_rebuild's exact
+    # minimum image (neighbor.cpp:134-141); owned atoms only
+    MVV2E = 1.0364269e-4
+
+    def md_set_state(self, vel, masses):
+        self.vel = np.array(vel, np.float64).reshape(-1, 3)
+        self.masses = np.asarray(masses, np.float64)
+
+    def md_get_state(self):
+        return self.xyz.copy(), self.vel.copy()
+
+    def kick(self, dt, drift=True, kicks=1):
+        o = slice(0, self.n_owned)
+        m = self.masses[self.species[o]][:, None]
+        k = (0.5 * dt) / (m * self.MVV2E)
+        f = self.f[o]
+        v = self.vel[o]
+        for _ in range(kicks):
+            v = v + f * k
+        self.vel[o] = v
+        if not drift:
+            return False
+        x = self.xyz[o] + v * dt
+        L = self.box
+        for ax in range(3):
+            if self.per[ax]:
+                c = x[:, ax] - L[ax] * np.floor(x[:, ax] / L[ax])
+                c = np.where(c < 0.0, c + L[ax], c)
+                x[:, ax] = np.where(c >= L[ax], c - L[ax], c)
+        self.xyz[o] = x
+        d = x - self.ref[o]
+        for ax in range(3):
+            if self.per[ax]:
+                far = np.abs(d[:, ax]) > 0.25 * L[ax]
+                d[far, ax] = d[far, ax] - L[ax] * np.floor(d[far, ax] / L[ax] + 0.5)
+        r2 = d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] + d[:, 2] * d[:, 2]
+        return bool(np.any(r2 > 0.25 * self.skin * self.skin))
+
+    def kinetic(self):
+        o = slice(0, self.n_owned)
+        m = self.masses[self.species[o]]
+        v = self.vel[o]
+        return float(np.sum(0.5 * m * (v * v).sum(axis=1) * self.MVV2E))
 
     def gather_positions(self, idx, out=None):
         t = torch.from_numpy(self.xyz[idx.numpy()].copy())
@@ -124,3 +170,70 @@ def test_slab_geometry_guards():
     assert s.near_right(x).tolist() == [False, False, False, True, True, False]
     assert Slab(0, 4, 40.0, 3.0).owner(np.array([-0.5, 0.0, 9.99, 10.0, 39.99, 40.0])).tolist() == \
         [3, 0, 0, 1, 3, 0]
+
+
+def _nve_worker(rank, world, port, steps, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1607_02904_b200 as tb
+        from oracle.oracle import Oracle
+        from paper_1607_02904_b200.parallel import Decomposition, SlabNVE, partition
+        c = _nve_case()
+        s = tb.make_diamond_lattice(5, 2, 2)
+        tb.init_velocities(s, 3000.0, 7)
+        halo = 3.2 + c.skin
+        gid = partition(c.xyz, c.box, world, rank, halo)
+        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo)
+        dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
+        nve = SlabNVE(dec, [28.0855], 3.2, c.skin)
+        nve.set_velocities(s.velocities[dec.gid])
+        samples = nve.run(steps, dt=0.001, thermo_every=10)
+        g, x, v = nve.owned_state()
+        parts = [None] * world
+        dist.all_gather_object(parts, (g, x, v))
+        migrated = [None] * world
+        dist.all_gather_object(migrated, dec.migrated)
+        if rank == 0:
+            n = len(c.xyz)
+            X, V = np.zeros((n, 3)), np.zeros((n, 3))
+            for g, x, v in parts:
+                X[g], V[g] = x, v
+            np.savez(out_path, x=X, v=V, samples=np.array(samples), rebuilds=nve.rebuilds,
+                     migrated=sum(migrated))
+    finally:
+        dist.destroy_process_group()
+
+
+def _nve_case():
+    import paper_1607_02904_b200 as tb
+    s = tb.make_diamond_lattice(5, 2, 2)
+    return systems.Case("nve_5x2x2", s.positions, s.species, s.box.lengths, s.box.periodic, 0.5,
+                        systems.si_text(tb))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_nve_matches_single_domain(tmp_path, world):
+    """SlabNVE (kick/drift of owned atoms, ghost exchange, rebuild vote,
+    migration at rebuilds) on a hot 160-atom lattice over 2 and 3 gloo ranks
+    follows the single-domain run of the same driver: atoms cross slab faces
+    and migrate, the rebuild schedule is identical, and positions, velocities
+    and energies agree to summation-order rounding."""
+    steps = 60
+    res = {}
+    for w in (1, world):
+        out = str(tmp_path / f"nve{w}.npz")
+        mp.spawn(_nve_worker, args=(w, _free_port(), steps, out), nprocs=w, join=True)
+        res[w] = np.load(out)
+    a, b = res[1], res[world]
+    assert int(a["rebuilds"]) >= 2 and int(b["rebuilds"]) == int(a["rebuilds"])
+    assert int(b["migrated"]) > 0                  # atoms did change owners
+    box = _nve_case().box
+    dx = b["x"] - a["x"]
+    dx -= box * np.round(dx / box)
+    assert np.abs(dx).max() < 1e-9
+    assert np.abs(b["v"] - a["v"]).max() < 1e-7
+    np.testing.assert_allclose(b["samples"], a["samples"], rtol=1e-10, atol=1e-9)
+    # energy is conserved by the distributed integrator
+    e = b["samples"][:, 1] + b["samples"][:, 2]
+    assert np.abs(e - e[0]).max() < 1e-3 * abs(e[0])
