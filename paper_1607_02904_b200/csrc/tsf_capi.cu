@@ -245,9 +245,24 @@ void evaluate_launches(Ctx& c, tsf::Precision p, std::uint32_t flags) {
   // in the register-limited force kernel.  Pairs beyond every cutoff of their
   // species pair are dropped here as well: they add exact zeros in the
   // reference (the kernel tests the same exact r^2).
-  tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
+  // atomic mode: the filter launch also zeroes the force accumulator (the
+  // f64/mixed double forces, or the f32 float partials)
+  void* zf = nullptr;
+  int zb = 0;
+  if (!(flags & TSF_DETERMINISTIC) && c.n > 0) {
+    if (p == tsf::Precision::F32) {
+      c.fself.reserve(3 * std::size_t(c.n) * sizeof(float) / sizeof(double) + 1);
+      zf = c.fself.get();
+      zb = 4;
+    } else {
+      zf = c.forces.get();
+      zb = 8;
+    }
+  }
+  tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair,
+                   zf, zb);
   c.mark(1);
-  tsf::compute(c, p, flags);
+  tsf::compute(c, p, zf ? (flags | tsf::kFlagForcesZeroed) : flags);
   c.mark(4);
 }
 

@@ -145,12 +145,17 @@ void list_build(Ctx& c, double cutoff, double skin);
 // reference's r_cut_max test (exports), or the per species-pair bounds the
 // force path uses (PairBounds; identical to Cutoff for one species).
 enum class FilterMode { Copy = 0, Cutoff = 1, Pair = 2 };
-void list_filter(Ctx& c, FilterMode mode);
+// zero_forces: optional [n][3] accumulator (zero_bytes = 8 double / 4 float)
+// the filter zeroes for the atomic-mode force kernel
+void list_filter(Ctx& c, FilterMode mode, void* zero_forces = nullptr, int zero_bytes = 0);
 bool list_needs_rebuild(Ctx& c);
 void snapshot_reference_positions(Ctx& c);
 
 // ---- kernels (tsf_force.cu) ----
 enum class Precision { F64 = 0, Mixed = 1, F32 = 2 };
+// compute() flag (internal, above the public TSF_* bits): the atomic-mode
+// force accumulator was zeroed by the filter launch
+constexpr std::uint32_t kFlagForcesZeroed = 1u << 16;
 void compute(Ctx& c, Precision prec, std::uint32_t flags);
 void upload_params(Ctx& c);
 

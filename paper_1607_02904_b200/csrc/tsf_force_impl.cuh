@@ -841,7 +841,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     } else {
       target = reinterpret_cast<Acc*>(c.forces.get());
     }
-    TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
+    if (!(flags & kFlagForcesZeroed))
+      TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
     a.forces = target;
     dispatch_spec<R, Acc, false>(c, a);
     if (kF32 && n > 0) {

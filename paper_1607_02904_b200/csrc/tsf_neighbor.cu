@@ -266,7 +266,8 @@ template <bool MULTI>
 __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
-    int* __restrict__ max_count, int* __restrict__ hist) {
+    int* __restrict__ max_count, int* __restrict__ hist, void* __restrict__ zero_f,
+    int zero_bytes) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
   const int ns = pb.ns;
@@ -280,6 +281,15 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
   __syncthreads();
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
+  // the force accumulator of the atomic-mode kernel that follows, zeroed here
+  // (this thread is waiting on its list anyway) instead of by a memset
+  if (zero_bytes == 8) {
+    double* z = static_cast<double*>(zero_f) + 3 * std::size_t(at);
+    z[0] = z[1] = z[2] = 0.0;
+  } else if (zero_bytes == 4) {
+    float* z = static_cast<float*>(zero_f) + 3 * std::size_t(at);
+    z[0] = z[1] = z[2] = 0.0f;
+  }
   const int m = skin_cnt[at];
   int w = 0;
   if (apply) {
@@ -554,7 +564,7 @@ void snapshot_reference_positions(Ctx& c) {
                            cudaMemcpyDeviceToDevice, c.stream));
 }
 
-void list_filter(Ctx& c, FilterMode mode) {
+void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes) {
   ListState& s = c.short_list;
   s.cap = c.skin_list.cap;
   s.nbr.reserve(std::size_t(s.cap) * c.npad + 1);
@@ -593,7 +603,7 @@ void list_filter(Ctx& c, FilterMode mode) {
     (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
         c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
-        c.flags.get() + 8);
+        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0);
     ++c.launches;
   }
   s.valid = true;
