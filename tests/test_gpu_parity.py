@@ -355,3 +355,33 @@ def test_lammps_style_table_gives_identical_results(tb, sic_text):
         ctx.close()
     for (e1, f1, w1), (e2, f2, w2) in zip(*out):
         assert e1 == e2 and np.array_equal(f1, f2) and np.array_equal(w1, w2)
+
+
+def test_graph_replay_follows_new_positions(tb, oracle):
+    """Steady-state evaluations replay a captured CUDA graph (evaluate() in
+    tsf_capi.cu): after set_positions (same list, no rebuild) the replay must
+    use the new positions — equal to a fresh context's eager evaluation (to
+    summation order) and to the oracle on the moved configuration."""
+    case = systems.perturbed(tb, 4, 0.12, 32, skin=0.5)
+    params, ctx = _ctx(tb, case)
+    for _ in range(3):                        # eager, capture, replay
+        ctx.compute("double", deterministic=True)
+    rng = np.random.default_rng(5)
+    moved = np.mod(case.xyz + rng.uniform(-0.05, 0.05, case.xyz.shape), case.box)
+    ctx.set_positions(moved)                  # within skin/2: no rebuild
+    e1, f1, w1 = ctx.compute("double", deterministic=True)   # a replay
+    e1b, f1b, _ = ctx.compute("double", deterministic=True)
+    assert e1 == e1b and np.array_equal(f1, f1b)
+    fresh = tb.Context(params, 0)             # its first evaluation is eager
+    fresh.set_system(moved, case.species, case.box, case.periodic)
+    fresh.set_neighbor_list(*ctx.export_neighbors("skin"), params.r_cut_max, case.skin)
+    e2, f2, w2 = fresh.compute("double", deterministic=True)
+    assert abs(e1 - e2) <= 1e-13 * abs(e2) and np.abs(f1 - f2).max() <= 1e-12
+    from oracle.oracle import parse_param_text
+    op = parse_param_text(case.params_text)
+    off, nb = ctx.export_neighbors("skin")
+    ref = oracle.compute_ref(op, moved, case.species, case.box, case.periodic, off, nb)
+    assert abs(e1 - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+    assert np.abs(f1 - ref["forces"]).max() <= F_TOL_D
+    for c in (ctx, fresh):
+        c.close()
