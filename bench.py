@@ -324,7 +324,9 @@ def main():
         from paper_1607_02904_b200.parallel import Decomposition, GpuEngine, partition
         halo = params.r_cut_max + skin
         eng = GpuEngine(params, local)
-        dec = Decomposition(eng, box, per, halo)
+        # ghost-centre mode (one exchange per step, no reverse force exchange)
+        # when the slabs are wide enough for its 2-halo ghost shell
+        dec = Decomposition(eng, box, per, halo, ghost_centers=box[0] / world >= 4 * halo)
         gid = partition(xyz, box, world, rank, halo)
         dec.setup(gid, xyz[gid], species[gid], params.r_cut_max, skin)
         ctx = eng.ctx

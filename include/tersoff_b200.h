@@ -145,6 +145,12 @@ int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset);
  * stream, not the legacy default stream's 0, to share ordering with a caller */
 int tsf_set_stream(tsf_ctx* ctx, void* stream);
 int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned);  /* default: all atoms */
+/* Ghost centers: user atoms [0, n_owned) are owned (energy, virial, MD);
+ * [n_owned, n_centers) are ghosts that still act as centers, so that every
+ * term putting force on an owned atom is evaluated locally and no reverse
+ * force exchange is needed (their energy is their owner's).  n_owned <=
+ * n_centers <= n; tsf_set_owned(n) is tsf_set_centers(n, n). */
+int tsf_set_centers(tsf_ctx* ctx, int64_t n_owned, int64_t n_centers);
 /* d_xyz[m][3] = positions of user atoms d_idx[0..m) */
 int tsf_gather_positions(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, double* d_xyz);
 /* positions of user atoms [lo, lo+m) = d_xyz[m][3] (ghost refresh) */

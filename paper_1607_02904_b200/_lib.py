@@ -82,6 +82,7 @@ PROTOTYPES = [
     ("tsf_profile_read", C.c_int, [_vp, _vp, _i64p, C.c_int]),
     ("tsf_set_stream", C.c_int, [_vp, _vp]),
     ("tsf_set_owned", C.c_int, [_vp, C.c_int64]),
+    ("tsf_set_centers", C.c_int, [_vp, C.c_int64, C.c_int64]),
     ("tsf_gather_positions", C.c_int, [_vp, _vp, C.c_int64, _vp]),
     ("tsf_scatter_positions", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
     ("tsf_gather_forces", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
@@ -111,6 +112,9 @@ def lib():
                         f"not be built ({exc}); there is no CPU fallback") from exc
             L = C.CDLL(LIB_PATH)
             for name, res, args in PROTOTYPES:
+                # an alternative build (TSF_LIBRARY, A/B experiments) may predate a symbol
+                if os.environ.get("TSF_LIBRARY") and not hasattr(L, name):
+                    continue
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args

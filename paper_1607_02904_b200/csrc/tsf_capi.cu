@@ -161,6 +161,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.n = n;
     c.sorted = false;
     c.n_owned = -1;
+    c.n_energy = -1;
     ++c.list_version;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
@@ -499,10 +500,21 @@ int tsf_set_stream(tsf_ctx* ctx, void* stream) {
   });
 }
 
+int tsf_set_centers(tsf_ctx* ctx, int64_t n_owned, int64_t n_centers) {
+  return guard(&ctx->c, [&] {
+    if (n_centers > ctx->c.n) throw tsf::ConfigError("center count exceeds the atom count");
+    if (n_owned > n_centers) throw tsf::ConfigError("owned count exceeds the center count");
+    ctx->c.n_owned = n_centers < 0 ? -1 : n_centers;
+    ctx->c.n_energy = n_owned < 0 ? -1 : n_owned;
+    ++ctx->c.list_version;
+  });
+}
+
 int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned) {
   return guard(&ctx->c, [&] {
     if (n_owned > ctx->c.n) throw tsf::ConfigError("owned count exceeds the atom count");
     ctx->c.n_owned = n_owned < 0 ? -1 : n_owned;
+    ctx->c.n_energy = -1;
     ++ctx->c.list_version;
     ctx->c.forces_current = false;
   });

@@ -71,6 +71,8 @@ struct Ctx {
   DevBuf<int> inv;             // [n] user index -> slot
   bool sorted = false;         // false: perm is the identity (slot == user index)
   std::int64_t n_owned = -1;   // user atoms [0, n_owned) are centers; -1: all
+  std::int64_t n_energy = -1;  // user atoms [0, n_energy) are owned: they count energy and
+                               // virial and are integrated by MD; -1: the centers
   cudaStream_t own_stream = nullptr;
   DevBuf<double4> pos;         // [n] slot order {x, y, z, species}
   DevBuf<float4> posf;         // [n] slot order float shadow for the cutoff pre-tests

@@ -56,6 +56,8 @@ struct ForceArgs {
   int n_owned;         // slots to cover (all local atoms)
   const int* perm;     // slot -> user index (nullptr: identity)
   int center_limit;    // only user atoms below this act as centers (ghosts above)
+  int energy_limit;    // only centers below this count energy and virial (owned atoms;
+                       // the ghost centers between them give the owned atoms' forces)
   int npad;
   Box box;
   const int* nbr;      // short list, ELL column-major
@@ -181,7 +183,7 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
 // then the two positions (stage B, dependent on stage A).
 struct TileIdx {
   int i, n, j;
-  bool ghost;   // a decomposition ghost: receives forces, is not a centre
+  bool ghost;     // a decomposition ghost: receives forces, is not a centre
 };
 
 // Resident blocks per SM the register allocation must allow (B200, si2m /
@@ -204,7 +206,7 @@ constexpr int kForceMinBlocks = G == 8 ? TSF_FORCE_MINB_F64_G8 : TSF_FORCE_MINB_
 template <int G>
 constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_FORCE_MINB_F32;
 
-template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF>
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FOREIGN = false>
 __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     k_force(const __grid_constant__ ForceArgs<R> a) {
 #ifndef TSF_CACHE_G16
@@ -257,6 +259,9 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   const int nwarps_total = gridDim.x * (kBlock / 32);
   const int last = a.n_owned - 1;
   const bool has_ghosts = a.center_limit < a.n_owned;
+  // ghost centres (tsf_set_centers) exist only in FOREIGN instantiations: a
+  // runtime test in the common kernel cost 1-2% (tools/ab.py)
+  const bool has_foreign = FOREIGN && a.energy_limit < a.center_limit;
 
   // stage A loads: count and this lane's list entry (clamped into range; the
   // entry past the count is unused, it only keeps the dependent load legal)
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     t.n = in ? a.cnt[t.i] : 0;
     const int v = in ? a.nbr[ell_at(gl, t.i, a.npad)] : 0;
     t.j = unsigned(v) <= unsigned(last) ? v : 0;
-    // ghost test two tiles ahead (its perm[] load at the tile start was 24%
+    // ghost tests two tiles ahead (the perm[] load at the tile start was 24%
     // of the stall samples, ncu); skipped when the context has no ghosts
     t.ghost = has_ghosts && in && (a.perm ? a.perm[t.i] : t.i) >= a.center_limit;
     return t;
@@ -288,12 +293,13 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   while (true) {
     int i, n_i, j;
     double4 pi, pj;
-    bool active;
+    bool active, foreign;
     if (OVF) {
       if (work * kPerWarp >= n_ovf) break;   // warp-uniform
       const int q = work * kPerWarp + lane / G;
       active = q < n_ovf;
       i = a.ovf_in[active ? q : work * kPerWarp];
+      foreign = has_foreign && (a.perm ? a.perm[i] : i) >= a.energy_limit;
       n_i = active ? a.cnt[i] : 0;
       j = gl < n_i ? a.nbr[ell_at(gl, i, a.npad)] : i;
       pi = a.pos[i];
@@ -304,6 +310,8 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       n_i = nxt.n;
       j = nxt.j;
       const bool ghost = nxt.ghost;
+      // a ghost centre (ghost-centre decompositions only: no load otherwise)
+      foreign = has_foreign && (a.perm ? a.perm[i] : i) >= a.energy_limit;
       pi = pi_n;
       pj = pj_n;
       // keep the pipeline full: positions of the next tile, list of the one after
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
                    Acc(rx * py), Acc(rx * pz), Acc(ry * pz)};
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
-        if (!slot) ev[q] = Acc(0);
+        if (!slot || (FOREIGN && foreign)) ev[q] = Acc(0);
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) ev[q] += __shfl_xor_sync(kFull, ev[q], o);
       }
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         for (int q = 0; q < 7; ++q) a.atom_ev[8 * std::size_t(i) + q] = double(ev[q]);
     }
     if (slot) {
-      if constexpr (!(OVF && DET)) {
+      if constexpr (!(OVF && DET)) if (!FOREIGN || !foreign) {   // ghost centres: forces only
         e_acc += Acc(v);
         const R rx = R(dx), ry = R(dy), rz = R(dz);
         w_acc[0] += Acc(rx * px);
@@ -697,10 +705,10 @@ int persistent_blocks(K kernel, int tiles) {
 
 constexpr int kOverflowBlocks = 4 * 148;   // per tier launch; idle tiers exit at once
 
-template <typename R, typename Acc, int G, int SPEC, bool DET>
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN>
 int launch_main(Ctx& c, ForceArgs<R> a) {
   const int tiles = std::max(1, ceil_div(a.n_owned, kBlock / G));
-  auto kern = k_force<R, Acc, G, SPEC, DET, false>;
+  auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN>;
   const int blocks = persistent_blocks(kern, tiles);
   a.partial_base = 0;
   c.mark(2);
@@ -710,8 +718,8 @@ int launch_main(Ctx& c, ForceArgs<R> a) {
   return blocks;
 }
 
-template <typename R, typename Acc, int SPEC, bool DET>
-void run_force(Ctx& c, ForceArgs<R> a) {
+template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN>
+void run_force_t(Ctx& c, ForceArgs<R> a) {
   // Group width from the short-count distribution of the last list build
   // (atoms over 4 / over 8); atoms over the width — or that outgrow it
   // between rebuilds — take the G=16 / G=32 tier launches.  Measured per-atom
@@ -744,10 +752,10 @@ void run_force(Ctx& c, ForceArgs<R> a) {
   a.ovf_out_count = a.flags + 1;
   int nb = 0;
   switch (g) {
-    case 4: nb = launch_main<R, Acc, 4, SPEC, DET>(c, a); break;
-    case 8: nb = launch_main<R, Acc, 8, SPEC, DET>(c, a); break;
-    case 16: nb = launch_main<R, Acc, 16, SPEC, DET>(c, a); break;
-    default: nb = launch_main<R, Acc, 32, SPEC, DET>(c, a); break;
+    case 4: nb = launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
+    case 8: nb = launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
+    case 16: nb = launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
+    default: nb = launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
   }
   auto tier = [&](auto kernel, int blocks, bool last) {
     a.partial_base = nb;
@@ -760,14 +768,14 @@ void run_force(Ctx& c, ForceArgs<R> a) {
     ++c.launches;
     if (!last) ++cur;
   };
-  if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true>, kOverflowBlocks, false);
-  if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true>, kOverflowBlocks, false);
+  if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
+  if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
   if (g < 32) {
-    tier(k_force<R, Acc, 32, SPEC, DET, true>, mx > 16 ? kOverflowBlocks : kOverflowBlocks / 4,
-         true);
+    tier(k_force<R, Acc, 32, SPEC, DET, true, FOREIGN>,
+         mx > 16 ? kOverflowBlocks : kOverflowBlocks / 4, true);
     if (DET) {
       k_queued_ev<<<kOverflowBlocks, kBlock, 0, c.stream>>>(
-          a.atom_ev, a.cnt, a.perm, a.n_owned, a.center_limit, g, a.flags + 1,
+          a.atom_ev, a.cnt, a.perm, a.n_owned, a.energy_limit, g, a.flags + 1,
           a.partials + std::size_t(nb) * kRedWidth);
       nb += kOverflowBlocks;
       ++c.launches;
@@ -775,6 +783,12 @@ void run_force(Ctx& c, ForceArgs<R> a) {
   }
   k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb, c.result.get());
   ++c.launches;
+}
+
+template <typename R, typename Acc, int SPEC, bool DET>
+void run_force(Ctx& c, const ForceArgs<R>& a) {
+  if (a.energy_limit < a.center_limit) run_force_t<R, Acc, SPEC, DET, true>(c, a);
+  else run_force_t<R, Acc, SPEC, DET, false>(c, a);
 }
 
 template <typename R, typename Acc, bool DET>
@@ -798,6 +812,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.n_owned = int(c.n);
   a.perm = c.sorted ? c.perm.get() : nullptr;
   a.center_limit = int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
+  a.energy_limit = c.n_energy >= 0 ? int(std::min<std::int64_t>(c.n_energy, a.center_limit))
+                                   : a.center_limit;
   a.npad = npad;
   a.box = c.box;
   a.nbr = c.short_list.nbr.get();

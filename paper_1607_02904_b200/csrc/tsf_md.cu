@@ -356,7 +356,8 @@ void unsort(Ctx& c) {
 }
 
 int center_limit(const Ctx& c) {   // user atoms below it are owned (all unless decomposed)
-  return int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
+  const std::int64_t centers = c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n;
+  return int(c.n_energy >= 0 ? std::min<std::int64_t>(c.n_energy, centers) : centers);
 }
 
 void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {

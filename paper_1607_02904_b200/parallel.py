@@ -90,9 +90,11 @@ class GpuEngine:
     def _p(self, t: torch.Tensor):
         return C.c_void_p(t.data_ptr())
 
-    def load(self, xyz: np.ndarray, species: np.ndarray, box, periodic, n_owned: int):
+    def load(self, xyz: np.ndarray, species: np.ndarray, box, periodic, n_owned: int,
+             n_centers: int = None):
         self.ctx.set_system(xyz, species, box, periodic)
-        self.ctx._ok(self._lib.tsf_set_owned(self.ctx._h, n_owned))
+        n_centers = n_owned if n_centers is None else n_centers
+        self.ctx._ok(self._lib.tsf_set_centers(self.ctx._h, n_owned, n_centers))
 
     def build(self, cutoff: float, skin: float):
         self.ctx.build_neighbor_list(cutoff, skin)
@@ -146,22 +148,36 @@ class GpuEngine:
 
 
 class Decomposition:
-    """One rank's view: owned atoms (global ids), ghost blocks, send lists."""
+    """One rank's view: owned atoms (global ids), ghost blocks, send lists.
 
-    def __init__(self, engine, box, periodic, halo: float, group=None):
+    ghost_centers=False (classic): ghosts within halo = r_cut_max + skin of a
+    face; only owned atoms are centres; the forces their terms put on ghosts
+    go back to the owners (reverse exchange).
+    ghost_centers=True: ghosts within 2 halo; the first layer (within halo)
+    also acts as centres (tsf_set_centers), so every term that puts force on
+    an owned atom is evaluated locally — one exchange per step instead of two,
+    for ~2 halo / slab of redundant compute; energy and virial stay with the
+    owners.  Local layout: [owned | layer-1 from left | layer-1 from right |
+    layer-2 from left | layer-2 from right]."""
+
+    def __init__(self, engine, box, periodic, halo: float, group=None,
+                 ghost_centers: bool = False):
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.box = np.asarray(box, np.float64)
         self.periodic = np.asarray(periodic, np.uint8)
+        self.ghost_centers = bool(ghost_centers)
+        reach = 2.0 * halo if self.ghost_centers else halo      # ghost selection distance
         if self.world > 1:
             if not self.periodic[0]:
                 raise ConfigError("slab decomposition needs a periodic x axis")
-            if self.box[0] / self.world < 2.0 * halo:
+            if self.box[0] / self.world < 2.0 * reach:
                 raise ConfigError(f"{self.world} slabs of {self.box[0] / self.world:.3f} A are "
-                                  f"thinner than 2 x halo = {2 * halo:.3f} A")
+                                  f"thinner than 2 x {reach:.3f} A")
         self.slab = Slab(self.rank, self.world, float(self.box[0]), float(halo))
+        self.slab_sel = Slab(self.rank, self.world, float(self.box[0]), float(reach))
         self.left = (self.rank - 1) % self.world
         self.right = (self.rank + 1) % self.world
         self.migrated = 0      # atoms received from neighbours by migrate()
@@ -179,14 +195,19 @@ class Decomposition:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
-    def _swap_counts(self, n_left: int, n_right: int):
+    def _swap_counts(self, n_left, n_right):
+        """Send count(s) left and right, return what the left and right
+        neighbours sent (ints, or tuples when tuples were sent)."""
         dev = self._device()
-        send_l = torch.tensor([n_left], dtype=torch.int64, device=dev)
-        send_r = torch.tensor([n_right], dtype=torch.int64, device=dev)
-        from_r = torch.zeros(1, dtype=torch.int64, device=dev)
-        from_l = torch.zeros(1, dtype=torch.int64, device=dev)
+        k = len(n_left) if isinstance(n_left, (tuple, list)) else 1
+        send_l = torch.tensor(n_left if k > 1 else [n_left], dtype=torch.int64, device=dev)
+        send_r = torch.tensor(n_right if k > 1 else [n_right], dtype=torch.int64, device=dev)
+        from_r = torch.zeros(k, dtype=torch.int64, device=dev)
+        from_l = torch.zeros(k, dtype=torch.int64, device=dev)
         self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
                        [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+        if k > 1:
+            return tuple(int(x) for x in from_l.tolist()), tuple(int(x) for x in from_r.tolist())
         return int(from_l.item()), int(from_r.item())
 
     # ---- setup at a (re)build -------------------------------------------
@@ -199,6 +220,7 @@ class Decomposition:
         species = np.ascontiguousarray(species[order], np.int32)
         self.n_owned = len(self.gid)
         dev = self._device()
+        self.n_gl1 = self.n_gr1 = 0              # layer-1 ghosts (ghost_centers)
         if self.world == 1:
             self.send_left = self.send_right = np.zeros(0, np.int64)
             self.n_gl = self.n_gr = 0
@@ -206,9 +228,16 @@ class Decomposition:
             gsp = np.zeros(0, np.int32)
             self.ghost_gid = np.zeros(0, np.int64)
         else:
-            self.send_left = np.nonzero(self.slab.near_left(xyz[:, 0]))[0]
-            self.send_right = np.nonzero(self.slab.near_right(xyz[:, 0]))[0]
-            self.n_gl, self.n_gr = self._swap_counts(len(self.send_left), len(self.send_right))
+            def select(near_sel, near_l1):
+                idx = np.nonzero(near_sel(xyz[:, 0]))[0]
+                l1 = near_l1(xyz[idx, 0])
+                return idx[np.argsort(~l1, kind="stable")], int(l1.sum())   # layer 1 first
+            self.send_left, nl1 = select(self.slab_sel.near_left, self.slab.near_left)
+            self.send_right, nr1 = select(self.slab_sel.near_right, self.slab.near_right)
+            (self.n_gl, self.n_gl1), (self.n_gr, self.n_gr1) = self._swap_counts(
+                (len(self.send_left), nl1), (len(self.send_right), nr1))
+            if not self.ghost_centers:
+                self.n_gl1 = self.n_gr1 = 0
             # ghost payload: global id, species, xyz (as float64 rows)
             def pack(idx):
                 return torch.from_numpy(np.column_stack([self.gid[idx].astype(np.float64),
@@ -219,14 +248,15 @@ class Decomposition:
             self._exchange([(pack(self.send_left), self.left, TAG_FWD_LEFT),
                             (pack(self.send_right), self.right, TAG_FWD_RIGHT)],
                            [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
-            ghosts = torch.cat([from_l, from_r]).cpu().numpy()
+            ghosts = torch.cat(self._layout(from_l, from_r)).cpu().numpy()
             self.ghost_gid = ghosts[:, 0].astype(np.int64)
             gsp = ghosts[:, 1].astype(np.int32)
             gxyz = np.ascontiguousarray(ghosts[:, 2:5])
         self.local_xyz = np.concatenate([xyz, gxyz])
         self.local_species = np.concatenate([species, gsp]).astype(np.int32)
+        self.n_centers = self.n_owned + self.n_gl1 + self.n_gr1
         self.engine.load(self.local_xyz, self.local_species, self.box, self.periodic,
-                         self.n_owned)
+                         self.n_owned, self.n_centers)
         self.engine.build(cutoff, skin)
         self.t_send_left = torch.from_numpy(self.send_left.astype(np.int32)).to(dev)
         self.t_send_right = torch.from_numpy(self.send_right.astype(np.int32)).to(dev)
@@ -251,12 +281,23 @@ class Decomposition:
         from_l, from_r = self._pos_from_l, self._pos_from_r
         self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
                        [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
-        self.engine.scatter_positions(self.n_owned, from_l)
-        self.engine.scatter_positions(self.n_owned + self.n_gl, from_r)
+        lo = self.n_owned
+        for block in self._layout(from_l, from_r):
+            self.engine.scatter_positions(lo, block)
+            lo += len(block)
+
+    def _layout(self, from_l, from_r):
+        """Received ghost rows in local order: classic [left | right];
+        ghost_centers [layer-1 left | layer-1 right | layer-2 left | layer-2 right]."""
+        if not self.ghost_centers:
+            return [from_l, from_r]
+        return [from_l[: self.n_gl1], from_r[: self.n_gr1], from_l[self.n_gl1:],
+                from_r[self.n_gr1:]]
 
     def reverse(self):
-        """Send ghost forces home and add them to the owners' forces."""
-        if self.world == 1:
+        """Send ghost forces home and add them to the owners' forces (classic
+        mode; with ghost_centers the owned forces are already complete)."""
+        if self.world == 1 or self.ghost_centers:
             return
         f_gl = self.engine.ghost_forces(self.n_owned, self.n_gl, out=self._f_ghost_l)
         f_gr = self.engine.ghost_forces(self.n_owned + self.n_gl, self.n_gr, out=self._f_ghost_r)

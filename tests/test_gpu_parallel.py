@@ -43,6 +43,38 @@ def test_owned_centres_match_oracle(tb, oracle):
             assert np.abs(f - ref["forces"]).max() <= ftol * max(1, np.abs(ref["forces"]).max())
 
 
+def test_ghost_centres_split_energy_from_forces(tb, oracle):
+    """tsf_set_centers(n_owned, n_centers): atoms [0, n_centers) act as
+    centres (forces from all their terms), only [0, n_owned) count energy and
+    virial — the ghost-centre decomposition's contract.  Also through the
+    tier launches (a perturbed lattice has 5-neighbour atoms) and both modes."""
+    from oracle.oracle import parse_param_text
+    c = systems.perturbed(tb, 4, 0.15, 17, skin=0.5)
+    n = len(c.xyz)
+    rng = np.random.default_rng(4)
+    order = rng.permutation(n)
+    xyz, sp = c.xyz[order], c.species[order]
+    n_owned, n_centers = 200, 380
+    op = parse_param_text(c.params_text)
+    off, nb = oracle.build_neighbor_list(xyz, c.box, c.periodic, op.r_cut_max, c.skin)
+    ref_f = oracle.compute_ref(op, xyz, sp, c.box, c.periodic, off, nb, n_center=n_centers)
+    ref_e = oracle.compute_ref(op, xyz, sp, c.box, c.periodic, off, nb, n_center=n_owned)
+    params = tb.builtin_silicon()
+    ctx = tb.Context(params, 0)
+    ctx.set_system(xyz, sp, c.box, c.periodic)
+    ctx.build_neighbor_list(params.r_cut_max, c.skin)
+    from paper_1607_02904_b200 import _lib as L
+    ctx._ok(L.lib().tsf_set_centers(ctx._h, n_owned, n_centers))
+    for det in (True, False):
+        for prec, etol, ftol in (("double", 1e-12, 1e-10), ("mixed", 1e-6, 1e-4)):
+            e, f, w = ctx.compute(prec, deterministic=det)
+            assert abs(e - ref_e["energy"]) <= etol * abs(ref_e["energy"])
+            assert np.abs(w - ref_e["virial"]).max() <= etol * 10 * np.abs(ref_e["virial"]).max()
+            fs = max(1, np.abs(ref_f["forces"]).max())
+            assert np.abs(f - ref_f["forces"]).max() <= ftol * fs
+    ctx.close()
+
+
 def test_gather_scatter_add(tb):
     import ctypes as C
     from paper_1607_02904_b200 import _lib as L
@@ -89,7 +121,7 @@ class _Mailbox:
             return self.q.setdefault((src, dst, tag), queue.Queue())
 
 
-def _emulated(tb, mail, rank, world, c, out):
+def _emulated(tb, mail, rank, world, c, out, ghost_centers=False):
     """One emulated rank: Decomposition with a mailbox exchange (host copies)."""
     from paper_1607_02904_b200 import parallel as P
     torch.cuda.set_device(0)
@@ -102,6 +134,8 @@ def _emulated(tb, mail, rank, world, c, out):
         dec.rank, dec.world = rank, world
         dec.box, dec.periodic = np.asarray(c.box), np.asarray(c.periodic, np.uint8)
         dec.slab = P.Slab(rank, world, float(c.box[0]), halo)
+        dec.ghost_centers = ghost_centers
+        dec.slab_sel = P.Slab(rank, world, float(c.box[0]), 2 * halo if ghost_centers else halo)
         dec.left, dec.right = (rank - 1) % world, (rank + 1) % world
 
         def exchange(sends, recvs):
@@ -121,15 +155,20 @@ def _emulated(tb, mail, rank, world, c, out):
                      len(dec.ghost_gid))
 
 
-def test_two_emulated_ranks_match_one_context(tb):
-    c = systems.perturbed(tb, 5, 0.12, 21, skin=0.5)
+@pytest.mark.parametrize("cells,ghost_centers", [(5, False), (6, True)])
+def test_two_emulated_ranks_match_one_context(tb, cells, ghost_centers):
+    """Two ranks emulated on one GPU (host mailbox exchange, no cross-rank
+    GPU waits), classic reverse-exchange mode and ghost-centre mode, against
+    one context on the whole system."""
+    c = systems.perturbed(tb, cells, 0.12, 21, skin=0.5)
     params = tb.builtin_silicon()
     ctx = tb.Context(params, 0)
     ctx.set_system(c.xyz, c.species, c.box, c.periodic)
     ctx.build_neighbor_list(params.r_cut_max, c.skin)
     e1, f1, w1 = ctx.compute("double", deterministic=True)
     mail, out = _Mailbox(), {}
-    threads = [threading.Thread(target=_emulated, args=(tb, mail, r, 2, c, out)) for r in range(2)]
+    threads = [threading.Thread(target=_emulated, args=(tb, mail, r, 2, c, out, ghost_centers))
+               for r in range(2)]
     for t in threads:
         t.start()
     for t in threads:

@@ -28,10 +28,11 @@ class OracleEngine:
         self.op = parse_param_text(params_text)
         self.device = torch.device("cpu")
 
-    def load(self, xyz, species, box, periodic, n_owned):
+    def load(self, xyz, species, box, periodic, n_owned, n_centers=None):
         self.xyz = np.array(xyz, np.float64)
         self.species = np.asarray(species, np.int32)
         self.box, self.per, self.n_owned = np.asarray(box), np.asarray(periodic), n_owned
+        self.n_centers = n_owned if n_centers is None else n_centers
 
     def build(self, cutoff, skin):
         self.off, self.nb = self.oracle.build_neighbor_list(self.xyz, self.box, self.per, cutoff,
@@ -91,9 +92,14 @@ class OracleEngine:
         self.xyz[lo:lo + len(t)] = t.numpy()
 
     def compute(self, precision="double", deterministic=False):
+        # forces from every centre (ghost centres included), energy and
+        # virial from the owned centres only — tsf_set_centers' semantics
         r = self.oracle.compute_ref(self.op, self.xyz, self.species, self.box, self.per, self.off,
-                                    self.nb, n_center=self.n_owned)
+                                    self.nb, n_center=self.n_centers)
         self.f = r["forces"].copy()
+        if self.n_centers != self.n_owned:
+            r = self.oracle.compute_ref(self.op, self.xyz, self.species, self.box, self.per,
+                                        self.off, self.nb, n_center=self.n_owned)
         self.ev = np.concatenate([[r["energy"]], r["virial"]])
 
     def ghost_forces(self, lo, m, out=None):
@@ -112,7 +118,7 @@ def _case(cells):
     return systems.perturbed(tb, cells, 0.15, 17, skin=0.5)
 
 
-def _worker(rank, world, port, cells, shift, out_path):
+def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -121,7 +127,8 @@ def _worker(rank, world, port, cells, shift, out_path):
         c = _case(cells)
         halo = 3.2 + c.skin
         gid = partition(c.xyz, c.box, world, rank, halo)
-        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo)
+        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo,
+                            ghost_centers=ghost_centers)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
         if shift is not None:
             # move owned atoms a little: the forward exchange must refresh ghosts
@@ -143,13 +150,19 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world,cells,shifted", [(2, 4, False), (2, 4, True), (3, 5, False)])
-def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted):
+@pytest.mark.parametrize("world,cells,shifted,ghost_centers", [
+    (2, 4, False, False), (2, 4, True, False), (3, 5, False, False),
+    (2, 6, True, True), (3, 9, False, True)])
+def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted, ghost_centers):
+    """Classic mode (reverse force exchange) and ghost-centre mode (layer-1
+    ghosts act as centres, no reverse exchange) both give the single-process
+    energy, forces and virial."""
     from oracle.oracle import parse_param_text
     c = _case(cells)
     shift = np.array([0.03, -0.02, 0.01]) if shifted else None
     out = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out, ghost_centers), nprocs=world,
+             join=True)
     res = np.load(out)
     op = parse_param_text(c.params_text)
     off, nb = oracle.build_neighbor_list(c.xyz, c.box, c.periodic, op.r_cut_max, c.skin)
@@ -172,19 +185,20 @@ def test_slab_geometry_guards():
         [3, 0, 0, 1, 3, 0]
 
 
-def _nve_worker(rank, world, port, steps, out_path):
+def _nve_worker(rank, world, port, steps, out_path, nx=5, ghost_centers=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_1607_02904_b200 as tb
         from oracle.oracle import Oracle
         from paper_1607_02904_b200.parallel import Decomposition, SlabNVE, partition
-        c = _nve_case()
-        s = tb.make_diamond_lattice(5, 2, 2)
+        c = _nve_case(nx)
+        s = tb.make_diamond_lattice(nx, 2, 2)
         tb.init_velocities(s, 3000.0, 7)
         halo = 3.2 + c.skin
         gid = partition(c.xyz, c.box, world, rank, halo)
-        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo)
+        dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo,
+                            ghost_centers=ghost_centers)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
         nve = SlabNVE(dec, [28.0855], 3.2, c.skin)
         nve.set_velocities(s.velocities[dec.gid])
@@ -205,15 +219,15 @@ def _nve_worker(rank, world, port, steps, out_path):
         dist.destroy_process_group()
 
 
-def _nve_case():
+def _nve_case(nx=5):
     import paper_1607_02904_b200 as tb
-    s = tb.make_diamond_lattice(5, 2, 2)
-    return systems.Case("nve_5x2x2", s.positions, s.species, s.box.lengths, s.box.periodic, 0.5,
-                        systems.si_text(tb))
+    s = tb.make_diamond_lattice(nx, 2, 2)
+    return systems.Case(f"nve_{nx}x2x2", s.positions, s.species, s.box.lengths, s.box.periodic,
+                        0.5, systems.si_text(tb))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_nve_matches_single_domain(tmp_path, world):
+@pytest.mark.parametrize("world,nx,ghost_centers", [(2, 5, False), (3, 5, False), (2, 6, True)])
+def test_slab_nve_matches_single_domain(tmp_path, world, nx, ghost_centers):
     """SlabNVE (kick/drift of owned atoms, ghost exchange, rebuild vote,
     migration at rebuilds) on a hot 160-atom lattice over 2 and 3 gloo ranks
     follows the single-domain run of the same driver: atoms cross slab faces
@@ -223,12 +237,13 @@ def test_slab_nve_matches_single_domain(tmp_path, world):
     res = {}
     for w in (1, world):
         out = str(tmp_path / f"nve{w}.npz")
-        mp.spawn(_nve_worker, args=(w, _free_port(), steps, out), nprocs=w, join=True)
+        mp.spawn(_nve_worker, args=(w, _free_port(), steps, out, nx, ghost_centers), nprocs=w,
+                 join=True)
         res[w] = np.load(out)
     a, b = res[1], res[world]
     assert int(a["rebuilds"]) >= 2 and int(b["rebuilds"]) == int(a["rebuilds"])
     assert int(b["migrated"]) > 0                  # atoms did change owners
-    box = _nve_case().box
+    box = _nve_case(nx).box
     dx = b["x"] - a["x"]
     dx -= box * np.round(dx / box)
     assert np.abs(dx).max() < 1e-9
