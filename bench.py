@@ -326,7 +326,9 @@ def main():
         eng = GpuEngine(params, local)
         # ghost-centre mode (one exchange per step, no reverse force exchange)
         # when the slabs are wide enough for its 2-halo ghost shell
-        dec = Decomposition(eng, box, per, halo, ghost_centers=box[0] / world >= 4 * halo)
+        # and the forward exchange overlapped with the interior centres' compute
+        dec = Decomposition(eng, box, per, halo, ghost_centers=box[0] / world >= 4 * halo,
+                            overlap=True)
         gid = partition(xyz, box, world, rank, halo)
         dec.setup(gid, xyz[gid], species[gid], params.r_cut_max, skin)
         ctx = eng.ctx

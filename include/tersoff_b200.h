@@ -151,6 +151,16 @@ int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned);  /* default: all atoms */
  * force exchange is needed (their energy is their owner's).  n_owned <=
  * n_centers <= n; tsf_set_owned(n) is tsf_set_centers(n, n). */
 int tsf_set_centers(tsf_ctx* ctx, int64_t n_owned, int64_t n_centers);
+/* Overlap of the halo exchange with compute: user atoms [0, n_interior) are
+ * owned atoms with no ghost within cutoff + skin (the caller's geometry); the
+ * next list build gives them slots [0, n_interior).  Then an evaluation may
+ * be split: tsf_compute_phase(.., 0) filters and computes those centres — no
+ * ghost position is read, so it can run while the ghosts are in flight — and
+ * tsf_compute_phase(.., 1) the rest, the tier launches and the reductions.
+ * Phase 0 does nothing (and phase 1 a whole evaluation) when the list has no
+ * split or the first evaluation after a build is due.  -1: off. */
+int tsf_set_interior(tsf_ctx* ctx, int64_t n_interior);
+int tsf_compute_phase(tsf_ctx* ctx, int precision, uint32_t flags, int phase);
 /* d_xyz[m][3] = positions of user atoms d_idx[0..m) */
 int tsf_gather_positions(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, double* d_xyz);
 /* positions of user atoms [lo, lo+m) = d_xyz[m][3] (ghost refresh) */

@@ -83,6 +83,8 @@ PROTOTYPES = [
     ("tsf_set_stream", C.c_int, [_vp, _vp]),
     ("tsf_set_owned", C.c_int, [_vp, C.c_int64]),
     ("tsf_set_centers", C.c_int, [_vp, C.c_int64, C.c_int64]),
+    ("tsf_set_interior", C.c_int, [_vp, C.c_int64]),
+    ("tsf_compute_phase", C.c_int, [_vp, C.c_int, C.c_uint32, C.c_int]),
     ("tsf_gather_positions", C.c_int, [_vp, _vp, C.c_int64, _vp]),
     ("tsf_scatter_positions", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
     ("tsf_gather_forces", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),

@@ -397,6 +397,18 @@ class Context:
                                        C.byref(moved) if check else None))
         return bool(moved.value)
 
+    def set_interior(self, n_interior: int):
+        """User atoms [0, n_interior) have no ghost within cutoff + skin;
+        the next list build lets evaluations split (tsf_set_interior)."""
+        self._ok(self._lib.tsf_set_interior(self._h, int(n_interior)))
+
+    def compute_phase(self, phase: int, precision: str = "double", deterministic: bool = False):
+        """Half of a split evaluation (tsf_compute_phase): 0 the interior
+        centres, 1 the rest and the reductions.  Results via the device."""
+        p = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
+        flags = L.TSF_DETERMINISTIC if deterministic else 0
+        self._ok(self._lib.tsf_compute_phase(self._h, p, flags, int(phase)))
+
     def md_kinetic(self) -> float:
         """Kinetic energy of the owned atoms, eV."""
         ke = C.c_double(0.0)

@@ -162,6 +162,8 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.sorted = false;
     c.n_owned = -1;
     c.n_energy = -1;
+    c.n_interior = -1;
+    c.split_slots = -1;
     ++c.list_version;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
@@ -237,8 +239,17 @@ void finish(Ctx& c, double* energy, double* forces, double* virial) {
     for (int q = 0; q < 6; ++q) virial[q] = res[1 + q];
 }
 
+void set_phase(Ctx& c, int lo, int hi, bool first, bool last) {
+  c.phase_lo = lo;
+  c.phase_hi = hi;
+  c.phase_first = first;
+  c.phase_last = last;
+}
+
 // One evaluation's device work: the short-list filter and the force launches.
 void evaluate_launches(Ctx& c, tsf::Precision p, std::uint32_t flags) {
+  set_phase(c, 0, int(c.n), true, true);
+  c.phase_blocks = 0;
   c.mark(0);
   // The short list is rebuilt from the skin list on every evaluation, as the
   // reference does (kernels.hpp:187-188).  A filter fused into the force
@@ -510,6 +521,50 @@ int tsf_set_centers(tsf_ctx* ctx, int64_t n_owned, int64_t n_centers) {
   });
 }
 
+int tsf_set_interior(tsf_ctx* ctx, int64_t n_interior) {
+  return guard(&ctx->c, [&] {
+    if (n_interior > ctx->c.n) throw tsf::ConfigError("interior count exceeds the atom count");
+    ctx->c.n_interior = n_interior < 0 ? -1 : n_interior;
+    ctx->c.split_slots = -1;     // takes effect with the next list build
+    ++ctx->c.list_version;
+  });
+}
+
+int tsf_compute_phase(tsf_ctx* ctx, int precision, uint32_t flags, int phase) {
+  return guard(&ctx->c, [&] {
+    Ctx& c = ctx->c;
+    if (precision < 0 || precision > 2) throw tsf::ConfigError("unknown precision selector");
+    if (phase != 0 && phase != 1) throw tsf::ConfigError("phase must be 0 or 1");
+    const tsf::Precision p = tsf::Precision(precision);
+    const int mode = int((flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
+    if (phase == 0) {
+      c.phase0_done = false;
+      if (!c.has_potential || !c.skin_list.valid) return;   // phase 1 reports it
+      const bool steady = !c.short_max_stale && c.short_apply == mode;
+      if (c.split_slots < 0 || !steady || c.profile) return;   // phase 1 does it all
+      const int split = int(c.split_slots);
+      set_phase(c, 0, split, true, false);
+      c.phase_blocks = 0;
+      tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, 0, split);
+      tsf::compute(c, p, flags);
+      c.phase0_done = true;
+      c.forces_current = false;
+      return;
+    }
+    if (!c.phase0_done) {          // no split (or not steady): one full evaluation
+      evaluate(c, p, flags);
+      return;
+    }
+    const int split = int(c.split_slots);
+    set_phase(c, split, int(c.n), false, true);
+    tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, split, int(c.n));
+    tsf::compute(c, p, flags);
+    set_phase(c, 0, int(c.n), true, true);
+    c.phase0_done = false;
+    c.forces_current = true;
+  });
+}
+
 int tsf_set_owned(tsf_ctx* ctx, int64_t n_owned) {
   return guard(&ctx->c, [&] {
     if (n_owned > ctx->c.n) throw tsf::ConfigError("owned count exceeds the atom count");
@@ -644,6 +699,7 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
     c.cutoff = cutoff;
     c.skin = skin;
     c.short_max_stale = true;
+    c.split_slots = -1;          // an external list: slots follow user order
     ++c.list_version;
     tsf::snapshot_reference_positions(c);
   });

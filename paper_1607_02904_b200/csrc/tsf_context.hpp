@@ -71,6 +71,9 @@ struct Ctx {
   DevBuf<int> inv;             // [n] user index -> slot
   bool sorted = false;         // false: perm is the identity (slot == user index)
   std::int64_t n_owned = -1;   // user atoms [0, n_owned) are centers; -1: all
+  std::int64_t n_interior = -1; // user atoms [0, n_interior) are interior owned atoms (no
+                               // ghost in their skin list): list builds give them slots
+                               // [0, n_interior) for the two-phase evaluation; -1: off
   std::int64_t n_energy = -1;  // user atoms [0, n_energy) are owned: they count energy and
                                // virial and are integrated by MD; -1: the centers
   cudaStream_t own_stream = nullptr;
@@ -113,6 +116,14 @@ struct Ctx {
                                // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
   DevBuf<int> overflow;        // [3n] tier queues (G = 8, 16, 32 inputs)
 
+  // slot range and position of the current compute() call in a two-phase
+  // evaluation (tsf_compute_phase); a plain evaluation is [0, n), first+last
+  int phase_lo = 0, phase_hi = 0;
+  bool phase_first = true, phase_last = true;
+  int phase_blocks = 0;                // partial blocks written by earlier phases
+  std::int64_t split_slots = -1;       // interior slots [0, split) of the current list
+  bool phase0_done = false;            // phase 0 ran; phase 1 completes the evaluation
+
   // CUDA graph of the steady-state evaluation (filter + force launches),
   // replayed while its key holds; see evaluate() in tsf_capi.cu
   std::uint64_t list_version = 0;      // bumped by every list / centre-set change
@@ -149,7 +160,9 @@ void list_build(Ctx& c, double cutoff, double skin);
 enum class FilterMode { Copy = 0, Cutoff = 1, Pair = 2 };
 // zero_forces: optional [n][3] accumulator (zero_bytes = 8 double / 4 float)
 // the filter zeroes for the atomic-mode force kernel
-void list_filter(Ctx& c, FilterMode mode, void* zero_forces = nullptr, int zero_bytes = 0);
+// lo / hi: the slot range (two-phase evaluation); hi < 0: all atoms
+void list_filter(Ctx& c, FilterMode mode, void* zero_forces = nullptr, int zero_bytes = 0,
+                 int lo = 0, int hi = -1);
 bool list_needs_rebuild(Ctx& c);
 void snapshot_reference_positions(Ctx& c);
 

@@ -53,7 +53,9 @@ struct ForceArgs {
   Row<R> row0;         // single-species row: read straight from the constant bank
   double cut0;
   const double4* pos;
-  int n_owned;         // slots to cover (all local atoms)
+  int n_owned;         // end of the slot range to cover (all local atoms: n)
+  int slot_base;       // start of the slot range (two-phase evaluation: 0 or n_interior)
+  int n_all;           // local atoms (neighbour indices lie in [0, n_all))
   const int* perm;     // slot -> user index (nullptr: identity)
   int center_limit;    // only user atoms below this act as centers (ghosts above)
   int energy_limit;    // only centers below this count energy and virial (owned atoms;
@@ -255,9 +257,9 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   const int gbase = tid - gl;          // block-local thread id of slot 0
   const int wbase = lane - gl;         // warp lane of slot 0
   constexpr int kAtomsPerBlock = kBlock / G;
-  const int ntiles = (a.n_owned + kAtomsPerBlock - 1) / kAtomsPerBlock;
+  const int ntiles = (a.n_owned - a.slot_base + kAtomsPerBlock - 1) / kAtomsPerBlock;
   const int nwarps_total = gridDim.x * (kBlock / 32);
-  const int last = a.n_owned - 1;
+  const int last = a.n_all - 1;
   const bool has_ghosts = a.center_limit < a.n_owned;
   // ghost centres (tsf_set_centers) exist only in FOREIGN instantiations: a
   // runtime test in the common kernel cost 1-2% (tools/ab.py)
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   // entry past the count is unused, it only keeps the dependent load legal)
   auto load_idx = [&](int tile) {
     TileIdx t;
-    t.i = tile * kAtomsPerBlock + tid / G;
+    t.i = a.slot_base + tile * kAtomsPerBlock + tid / G;
     const bool in = tile < ntiles && t.i < a.n_owned;
     if (!in) t.i = 0;
     t.n = in ? a.cnt[t.i] : 0;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       pi_n = a.pos[nxt.i];
       pj_n = a.pos[nxt.j];
       nxt2 = load_idx(work + 2 * gridDim.x);
-      active = work * kAtomsPerBlock + tid / G < a.n_owned;
+      active = a.slot_base + work * kAtomsPerBlock + tid / G < a.n_owned;
       // ghost copies (decomposition) receive forces but are not centers
       if (active && ghost) {
         if (DET && gl == 0) {
@@ -707,10 +709,9 @@ constexpr int kOverflowBlocks = 4 * 148;   // per tier launch; idle tiers exit a
 
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN>
 int launch_main(Ctx& c, ForceArgs<R> a) {
-  const int tiles = std::max(1, ceil_div(a.n_owned, kBlock / G));
+  const int tiles = std::max(1, ceil_div(a.n_owned - a.slot_base, kBlock / G));
   auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN>;
   const int blocks = persistent_blocks(kern, tiles);
-  a.partial_base = 0;
   c.mark(2);
   kern<<<blocks, kBlock, 0, c.stream>>>(a);
   c.mark(3);
@@ -750,13 +751,19 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   int cur = 0;                              // queue the main launch fills
   a.ovf_out = g < 32 ? qbuf : nullptr;
   a.ovf_out_count = a.flags + 1;
-  int nb = 0;
+  // two-phase evaluation: the partials of the first phase's main launch
+  // precede this one's; tiers and the reduction run with the last phase
+  a.partial_base = c.phase_blocks;
+  int nb = c.phase_blocks;
   switch (g) {
-    case 4: nb = launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
-    case 8: nb = launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
-    case 16: nb = launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
-    default: nb = launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
+    case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
+    case 8: nb += launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
+    case 16: nb += launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
+    default: nb += launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
   }
+  c.phase_blocks = nb;
+  if (!c.phase_last) return;
+  c.phase_blocks = 0;
   auto tier = [&](auto kernel, int blocks, bool last) {
     a.partial_base = nb;
     a.ovf_in = qbuf + std::size_t(cur) * c.n;
@@ -809,7 +816,9 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.row0 = make_row<R>(c.params.entry(0, 0, 0));
   a.cut0 = c.params.entry(0, 0, 0).cutoff() * c.params.entry(0, 0, 0).cutoff();
   a.pos = c.pos.get();
-  a.n_owned = int(c.n);
+  a.slot_base = c.phase_lo;
+  a.n_owned = c.phase_hi;
+  a.n_all = int(c.n);
   a.perm = c.sorted ? c.perm.get() : nullptr;
   a.center_limit = int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
   a.energy_limit = c.n_energy >= 0 ? int(std::min<std::int64_t>(c.n_energy, a.center_limit))
@@ -826,7 +835,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   c.overflow.reserve(std::max<std::size_t>(3 * n, 1));
   c.partials.reserve(std::size_t(32 * 148 + 4 * kOverflowBlocks + 8) * kRedWidth);
   a.partials = c.partials.get();
-  TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));
+  if (c.phase_first) TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));
 
   constexpr bool kF32 = std::is_same<Acc, float>::value;
   if (det) {
@@ -842,7 +851,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     c.atom_ev.reserve(8 * n + 1);
     a.atom_ev = c.atom_ev.get();
     dispatch_spec<R, Acc, true>(c, a);
-    if (n > 0) {
+    if (n > 0 && c.phase_last) {
       k_gather<Acc><<<ceil_div(n, kBlock), kBlock, 0, c.stream>>>(
           int(n), npad, a.nbr, a.cnt, static_cast<const Acc*>(a.slot_x),
           static_cast<const Acc*>(a.slot_y), static_cast<const Acc*>(a.slot_z),
@@ -857,11 +866,11 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     } else {
       target = reinterpret_cast<Acc*>(c.forces.get());
     }
-    if (!(flags & kFlagForcesZeroed))
+    if (!(flags & kFlagForcesZeroed) && c.phase_first)
       TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
     a.forces = target;
     dispatch_spec<R, Acc, false>(c, a);
-    if (kF32 && n > 0) {
+    if (kF32 && n > 0 && c.phase_last) {
       k_to_double<<<ceil_div(3 * n, 256), 256, 0, c.stream>>>(
           reinterpret_cast<const float*>(target), c.forces.get(), 3 * n);
       ++c.launches;

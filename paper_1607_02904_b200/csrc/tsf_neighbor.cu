@@ -54,8 +54,12 @@ __device__ __forceinline__ void warp_atomic_max(int* p, int v) {
 }
 
 // Sort key (cell, user index) per slot; counts per cell; largest occupancy.
+// With an interior split (n_int >= 0, the decomposition's overlap mode) the
+// key is class-major: user atoms below n_int (interior owned) sort first, so
+// their slots are [0, n_int); the "cell" index is then class * ncells + cell,
+// keeping every (class, cell) run contiguous for the skin build.
 __global__ void k_cell_key(const double4* __restrict__ pos, const int* __restrict__ perm, int n,
-                           CellGrid g, unsigned long long* __restrict__ keys,
+                           CellGrid g, int n_int, unsigned long long* __restrict__ keys,
                            int* __restrict__ vals, int* __restrict__ count,
                            int* __restrict__ max_occ) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -64,8 +68,10 @@ __global__ void k_cell_key(const double4* __restrict__ pos, const int* __restric
   const int cx = clamp_cell(p.x, g.org[0], g.ext[0], g.nc[0]);
   const int cy = clamp_cell(p.y, g.org[1], g.ext[1], g.nc[1]);
   const int cz = clamp_cell(p.z, g.org[2], g.ext[2], g.nc[2]);
-  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx;
   const unsigned user = unsigned(perm ? perm[s] : s);
+  const int ncells = g.nc[0] * g.nc[1] * g.nc[2];
+  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx +
+                (n_int >= 0 && int(user) >= n_int ? ncells : 0);
   keys[s] = (static_cast<unsigned long long>(c) << 32) | user;
   vals[s] = s;
   warp_atomic_max(max_occ, atomicAdd(count + c, 1) + 1);
@@ -126,6 +132,7 @@ struct ListArgs {
   CellGrid g;
   const int* cell_of;
   const int* start;
+  int ncls;          // slot classes (1, or 2 with an interior split)
 };
 
 // Skin list, one thread per slot: candidates are the stencil cells' slot
@@ -143,7 +150,8 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
   const CellGrid& g = a.g;
   const float4 pfa = a.posf[at];
   const WrapF wrap = wrap_of(a.boxf);
-  const int home = a.cell_of[at];
+  const int ncells = g.nc[0] * g.nc[1] * g.nc[2];
+  const int home = a.cell_of[at] % ncells;   // class-major index when split
   const int cx = home % g.nc[0], cy = (home / g.nc[0]) % g.nc[1];
   const int cz = home / (g.nc[0] * g.nc[1]);
   int sx[3], sy[3], sz[3];
@@ -152,8 +160,10 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
   const int mz = axis_stencil(cz, g.nc[2], a.box.per[2], sz);
   int buf[CAP];
   int m = 0;
-  for (int q = 0; q < mx * my * mz; ++q) {
-    const int c = (sz[q / (mx * my)] * g.nc[1] + sy[(q / mx) % my]) * g.nc[0] + sx[q % mx];
+  for (int q = 0; q < mx * my * mz * a.ncls; ++q) {
+    const int qc = q % (mx * my * mz);
+    const int c = (sz[qc / (mx * my)] * g.nc[1] + sy[(qc / mx) % my]) * g.nc[0] + sx[qc % mx] +
+                  (q / (mx * my * mz)) * ncells;
     const int b1 = a.start[c + 1];
     for (int b = a.start[c]; b < b1; ++b) {
       if (b == at) continue;
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
     int* __restrict__ max_count, int* __restrict__ hist, void* __restrict__ zero_f,
-    int zero_bytes) {
+    int zero_bytes, int slot_lo, int slot_hi) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
   const int ns = pb.ns;
@@ -279,8 +289,8 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     sc2[threadIdx.x] = pb.c2[threadIdx.x];
   }
   __syncthreads();
-  const int at = blockIdx.x * blockDim.x + threadIdx.x;
-  if (at >= a.n) return;
+  const int at = slot_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (at >= slot_hi) return;
   // the force accumulator of the atomic-mode kernel that follows, zeroed here
   // (this thread is waiting on its list anyway) instead of by a memset
   if (zero_bytes == 8) {
@@ -406,6 +416,7 @@ ListArgs list_args(Ctx& c) {
   a.g = c.grid;
   a.cell_of = c.cell_of.get();
   a.start = c.cell_start.get();
+  a.ncls = c.n_interior >= 0 ? 2 : 1;
   return a;
 }
 
@@ -472,7 +483,8 @@ void list_build(Ctx& c, double cutoff, double skin) {
     g.ext[ax] = hi[ax] - lo[ax];
     g.nc[ax] = std::max(1, int(std::floor(g.ext[ax] / bc)));
   }
-  const std::int64_t ncells = std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2];
+  const std::int64_t ncells =
+      std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2] * (c.n_interior >= 0 ? 2 : 1);
   if (ncells > (1ll << 30)) throw ConfigError("cell grid too large");
 
   // ---- re-sort the atoms by (cell, user index) ----
@@ -501,7 +513,8 @@ void list_build(Ctx& c, double cutoff, double skin) {
   TSF_CUDA(cudaMemsetAsync(c.flags.get() + 6, 0, sizeof(int), c.stream));
   if (n > 0) {
     k_cell_key<<<blocks_for(n), kBlock, 0, c.stream>>>(
-        c.pos.get(), c.sorted ? c.perm.get() : nullptr, n, g, c.sort_keys.get(),
+        c.pos.get(), c.sorted ? c.perm.get() : nullptr, n, g,
+        c.n_interior >= 0 ? int(std::min<std::int64_t>(c.n_interior, n)) : -1, c.sort_keys.get(),
         c.sort_vals.get(), c.cell_count.get(), c.flags.get() + 6);
     ++c.launches;
     TSF_CUDA(cub::DeviceRadixSort::SortPairs(c.scan_tmp.get(), t_sort, c.sort_keys.get(),
@@ -556,6 +569,8 @@ void list_build(Ctx& c, double cutoff, double skin) {
   c.short_max_stale = true;
   c.short_list.valid = false;
   ++c.list_version;
+  // interior atoms hold slots [0, n_interior) after a split build
+  c.split_slots = c.n_interior >= 0 ? std::min<std::int64_t>(c.n_interior, n) : -1;
 }
 
 void snapshot_reference_positions(Ctx& c) {
@@ -564,7 +579,8 @@ void snapshot_reference_positions(Ctx& c) {
                            cudaMemcpyDeviceToDevice, c.stream));
 }
 
-void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes) {
+void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int lo, int hi) {
+  if (hi < 0) hi = int(c.n);
   ListState& s = c.short_list;
   s.cap = c.skin_list.cap;
   s.nbr.reserve(std::size_t(s.cap) * c.npad + 1);
@@ -600,10 +616,11 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes) {
     // (a TMA-staged, persistent variant measured slower: 0.138 vs 0.114 ms at
     // 2M atoms — its staging buffers take the L1 the position gathers hit,
     // 58% -> 9% hit rate)
-    (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
+    (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(std::max(hi - lo, 1)), kBlock, 0,
+                                                       c.stream>>>(
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
         c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
-        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0);
+        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi);
     ++c.launches;
   }
   s.valid = true;

@@ -91,10 +91,14 @@ class GpuEngine:
         return C.c_void_p(t.data_ptr())
 
     def load(self, xyz: np.ndarray, species: np.ndarray, box, periodic, n_owned: int,
-             n_centers: int = None):
+             n_centers: int = None, n_interior: int = -1):
         self.ctx.set_system(xyz, species, box, periodic)
         n_centers = n_owned if n_centers is None else n_centers
         self.ctx._ok(self._lib.tsf_set_centers(self.ctx._h, n_owned, n_centers))
+        self.ctx.set_interior(n_interior)
+
+    def compute_phase(self, phase: int, precision: str = "double", deterministic: bool = False):
+        self.ctx.compute_phase(phase, precision, deterministic)
 
     def build(self, cutoff: float, skin: float):
         self.ctx.build_neighbor_list(cutoff, skin)
@@ -161,7 +165,7 @@ class Decomposition:
     layer-2 from left | layer-2 from right]."""
 
     def __init__(self, engine, box, periodic, halo: float, group=None,
-                 ghost_centers: bool = False):
+                 ghost_centers: bool = False, overlap: bool = False):
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -169,6 +173,9 @@ class Decomposition:
         self.box = np.asarray(box, np.float64)
         self.periodic = np.asarray(periodic, np.uint8)
         self.ghost_centers = bool(ghost_centers)
+        # overlap: the forward exchange is in flight while the interior
+        # centres (no ghost within halo: slots [0, n_interior)) are computed
+        self.overlap = bool(overlap)
         reach = 2.0 * halo if self.ghost_centers else halo      # ghost selection distance
         if self.world > 1:
             if not self.periodic[0]:
@@ -186,14 +193,20 @@ class Decomposition:
     def _device(self):
         return getattr(self.engine, "device", torch.device("cpu"))
 
-    def _exchange(self, sends, recvs):
+    def _exchange_start(self, sends, recvs):
         """sends: [(tensor, dst, tag)], recvs: [(tensor, src, tag)] in a fixed
-        order on every rank (NCCL matches per pair in issue order, gloo by tag)."""
+        order on every rank (NCCL matches per pair in issue order, gloo by tag).
+        Returns the pending requests (NCCL: enqueued behind the current stream)."""
         ops = [dist.P2POp(dist.isend, t, d, self.group, tag) for t, d, tag in sends if t.numel()]
         ops += [dist.P2POp(dist.irecv, t, s, self.group, tag) for t, s, tag in recvs if t.numel()]
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def _exchange_finish(self, reqs):
+        for req in reqs:
+            req.wait()
+
+    def _exchange(self, sends, recvs):
+        self._exchange_finish(self._exchange_start(sends, recvs))
 
     def _swap_counts(self, n_left, n_right):
         """Send count(s) left and right, return what the left and right
@@ -213,8 +226,18 @@ class Decomposition:
     # ---- setup at a (re)build -------------------------------------------
     def setup(self, gid: np.ndarray, xyz: np.ndarray, species: np.ndarray, cutoff: float,
               skin: float):
-        """gid/xyz/species: this rank's owned atoms (global ids, global frame)."""
-        order = np.argsort(gid, kind="stable")
+        """gid/xyz/species: this rank's owned atoms (global ids, global frame).
+        Owned atoms are stored by (boundary, gid): interior ones — farther
+        than one halo from both faces, so no ghost in their lists — first.
+        self.last_order is the permutation applied to the inputs."""
+        if self.world > 1 and self.overlap:
+            boundary = self.slab.near_left(xyz[:, 0]) | self.slab.near_right(xyz[:, 0])
+            order = np.lexsort((gid, boundary))
+            self.n_interior = int((~boundary).sum())
+        else:
+            order = np.argsort(gid, kind="stable")
+            self.n_interior = -1
+        self.last_order = order
         self.gid = np.ascontiguousarray(gid[order], np.int64)
         xyz = np.ascontiguousarray(xyz[order], np.float64)
         species = np.ascontiguousarray(species[order], np.int32)
@@ -256,7 +279,7 @@ class Decomposition:
         self.local_species = np.concatenate([species, gsp]).astype(np.int32)
         self.n_centers = self.n_owned + self.n_gl1 + self.n_gr1
         self.engine.load(self.local_xyz, self.local_species, self.box, self.periodic,
-                         self.n_owned, self.n_centers)
+                         self.n_owned, self.n_centers, self.n_interior)
         self.engine.build(cutoff, skin)
         self.t_send_left = torch.from_numpy(self.send_left.astype(np.int32)).to(dev)
         self.t_send_right = torch.from_numpy(self.send_right.astype(np.int32)).to(dev)
@@ -309,8 +332,25 @@ class Decomposition:
         self.engine.add_forces(self.t_send_right, to_r)
 
     def evaluate(self, precision: str = "double", deterministic: bool = False):
-        self.forward()
-        self.engine.compute(precision, deterministic)
+        if self.overlap and self.world > 1:
+            # ghosts in flight while the interior centres compute (phase 0;
+            # a no-op when the engine cannot split yet — phase 1 then does it all)
+            send_l = self.engine.gather_positions(self.t_send_left, out=self._pos_send_l)
+            send_r = self.engine.gather_positions(self.t_send_right, out=self._pos_send_r)
+            from_l, from_r = self._pos_from_l, self._pos_from_r
+            reqs = self._exchange_start(
+                [(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
+                [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+            self.engine.compute_phase(0, precision, deterministic)
+            self._exchange_finish(reqs)
+            lo = self.n_owned
+            for block in self._layout(from_l, from_r):
+                self.engine.scatter_positions(lo, block)
+                lo += len(block)
+            self.engine.compute_phase(1, precision, deterministic)
+        else:
+            self.forward()
+            self.engine.compute(precision, deterministic)
         self.reverse()
 
     # ---- atom migration at a rebuild ----------------------
@@ -323,7 +363,7 @@ class Decomposition:
         species = self.local_species[: self.n_owned]
         if self.world == 1:
             self.setup(self.gid, xyz, species, cutoff, skin)
-            return np.asarray(vel, np.float64)
+            return np.asarray(vel, np.float64)[self.last_order]
         owner = self.slab.owner(xyz[:, 0])
         to_l = owner == self.left
         to_r = (owner == self.right) & ~to_l
@@ -347,9 +387,8 @@ class Decomposition:
         sp = np.concatenate([species[stay], arr[:, 1].astype(np.int32)])
         x = np.concatenate([xyz[stay], arr[:, 2:5]])
         v = np.concatenate([vel[stay], arr[:, 5:8]])
-        order = np.argsort(gid, kind="stable")
-        self.setup(gid[order], x[order], sp[order], cutoff, skin)
-        return v[order]
+        self.setup(gid, x, sp, cutoff, skin)
+        return v[self.last_order]
 
     def gather_results(self, total_atoms: int):
         """Energy/virial summed over ranks and global-order forces on rank 0

@@ -121,7 +121,7 @@ class _Mailbox:
             return self.q.setdefault((src, dst, tag), queue.Queue())
 
 
-def _emulated(tb, mail, rank, world, c, out, ghost_centers=False):
+def _emulated(tb, mail, rank, world, c, out, ghost_centers=False, overlap=False):
     """One emulated rank: Decomposition with a mailbox exchange (host copies)."""
     from paper_1607_02904_b200 import parallel as P
     torch.cuda.set_device(0)
@@ -134,7 +134,7 @@ def _emulated(tb, mail, rank, world, c, out, ghost_centers=False):
         dec.rank, dec.world = rank, world
         dec.box, dec.periodic = np.asarray(c.box), np.asarray(c.periodic, np.uint8)
         dec.slab = P.Slab(rank, world, float(c.box[0]), halo)
-        dec.ghost_centers = ghost_centers
+        dec.ghost_centers, dec.overlap = ghost_centers, overlap
         dec.slab_sel = P.Slab(rank, world, float(c.box[0]), 2 * halo if ghost_centers else halo)
         dec.left, dec.right = (rank - 1) % world, (rank + 1) % world
 
@@ -146,17 +146,21 @@ def _emulated(tb, mail, rank, world, c, out, ghost_centers=False):
                 t.copy_(mail.box(src, rank, tag).get(timeout=60).to(t.device))
             torch.cuda.current_stream().synchronize()
         dec._exchange = exchange
+        dec._exchange_start = lambda sends, recvs: exchange(sends, recvs) or []
+        dec._exchange_finish = lambda reqs: None
         gid = P.partition(c.xyz, c.box, world, rank, halo)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
-        dec.evaluate("double", deterministic=True)
+        dec.evaluate("double", deterministic=True)   # first after a build: single phase
+        dec.evaluate("double", deterministic=True)   # steady state: split when overlapping
         ev, f = eng.results()
         torch.cuda.current_stream().synchronize()
         out[rank] = (dec.gid, f[: dec.n_owned].cpu().numpy(), ev.cpu().numpy(),
                      len(dec.ghost_gid))
 
 
-@pytest.mark.parametrize("cells,ghost_centers", [(5, False), (6, True)])
-def test_two_emulated_ranks_match_one_context(tb, cells, ghost_centers):
+@pytest.mark.parametrize("cells,ghost_centers,overlap", [(5, False, False), (6, True, False),
+                                                          (6, True, True), (5, False, True)])
+def test_two_emulated_ranks_match_one_context(tb, cells, ghost_centers, overlap):
     """Two ranks emulated on one GPU (host mailbox exchange, no cross-rank
     GPU waits), classic reverse-exchange mode and ghost-centre mode, against
     one context on the whole system."""
@@ -167,7 +171,8 @@ def test_two_emulated_ranks_match_one_context(tb, cells, ghost_centers):
     ctx.build_neighbor_list(params.r_cut_max, c.skin)
     e1, f1, w1 = ctx.compute("double", deterministic=True)
     mail, out = _Mailbox(), {}
-    threads = [threading.Thread(target=_emulated, args=(tb, mail, r, 2, c, out, ghost_centers))
+    threads = [threading.Thread(target=_emulated,
+                                args=(tb, mail, r, 2, c, out, ghost_centers, overlap))
                for r in range(2)]
     for t in threads:
         t.start()
@@ -218,3 +223,46 @@ def test_slab_nve_single_rank_matches_md_run(tb):
     dx -= s.box.lengths * np.round(dx / s.box.lengths)
     assert np.abs(dx).max() < 1e-10
     assert np.abs(v - v_ref).max() < 1e-8
+
+
+def test_split_evaluation_matches_single_phase(tb):
+    """tsf_set_interior + tsf_compute_phase(0) then (1): the interior slots'
+    centres first, the rest after — the same forces as the context's own
+    one-phase evaluation (bitwise, deterministic mode) and energy/virial
+    (summation order)."""
+    c = systems.perturbed(tb, 4, 0.15, 17, skin=0.5)
+    params = tb.builtin_silicon()
+    ref = tb.Context(params, 0)
+    ref.set_system(c.xyz, c.species, c.box, c.periodic)
+    ref.build_neighbor_list(params.r_cut_max, c.skin)
+    ctx = tb.Context(params, 0)
+    ctx.set_system(c.xyz, c.species, c.box, c.periodic)
+    ctx.set_interior(200)                      # any split is valid without ghosts
+    ctx.build_neighbor_list(params.r_cut_max, c.skin)
+    import ctypes as C
+    from paper_1607_02904_b200 import _lib as L
+    for det in (True, False):
+        for prec in ("double", "mixed"):
+            e1, f1, w1 = ref.compute(prec, deterministic=det)
+            ctx._ok(L.lib().tsf_set_interior(ctx._h, 200))   # re-arms: next build / evaluation
+            ctx.build_neighbor_list(params.r_cut_max, c.skin)
+            e0, f0, _ = ctx.compute(prec, deterministic=det)  # after a build: one phase
+            ctx.compute_phase(0, prec, deterministic=det)
+            ctx.compute_phase(1, prec, deterministic=det)
+            ev = torch.empty(7, dtype=torch.float64, device="cuda:0")
+            fd = torch.empty((len(c.xyz), 3), dtype=torch.float64, device="cuda:0")
+            ctx._ok(L.lib().tsf_results_device(ctx._h, C.c_void_p(ev.data_ptr()),
+                                               C.c_void_p(fd.data_ptr())))
+            torch.cuda.synchronize(torch.device("cuda:0"))   # device-wide: the context's stream too
+            ev, f2 = ev.cpu().numpy(), fd.cpu().numpy()
+            tol = 1e-12 if prec == "double" else 1e-6
+            assert abs(ev[0] - e1) <= tol * abs(e1)
+            np.testing.assert_allclose(ev[1:7], w1, rtol=tol, atol=tol * np.abs(w1).max())
+            # same context, same slot layout: deterministic forces are bitwise
+            # the one-phase result; against `ref` (another slot order) to rounding
+            if det:
+                assert np.array_equal(f2, f0)
+            assert np.abs(f2 - f1).max() <= (1e-12 if prec == "double" else 1e-6) * \
+                max(1, np.abs(f1).max())
+    ref.close()
+    ctx.close()

@@ -28,7 +28,7 @@ class OracleEngine:
         self.op = parse_param_text(params_text)
         self.device = torch.device("cpu")
 
-    def load(self, xyz, species, box, periodic, n_owned, n_centers=None):
+    def load(self, xyz, species, box, periodic, n_owned, n_centers=None, n_interior=-1):
         self.xyz = np.array(xyz, np.float64)
         self.species = np.asarray(species, np.int32)
         self.box, self.per, self.n_owned = np.asarray(box), np.asarray(periodic), n_owned
@@ -102,6 +102,10 @@ class OracleEngine:
                                         self.off, self.nb, n_center=self.n_owned)
         self.ev = np.concatenate([[r["energy"]], r["virial"]])
 
+    def compute_phase(self, phase, precision="double", deterministic=False):
+        if phase == 1:             # the oracle has no split: the whole step in phase 1
+            self.compute(precision, deterministic)
+
     def ghost_forces(self, lo, m, out=None):
         t = torch.from_numpy(self.f[lo:lo + m].copy())
         return out.copy_(t) if out is not None else t
@@ -118,7 +122,7 @@ def _case(cells):
     return systems.perturbed(tb, cells, 0.15, 17, skin=0.5)
 
 
-def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False):
+def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -128,7 +132,7 @@ def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False):
         halo = 3.2 + c.skin
         gid = partition(c.xyz, c.box, world, rank, halo)
         dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo,
-                            ghost_centers=ghost_centers)
+                            ghost_centers=ghost_centers, overlap=overlap)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
         if shift is not None:
             # move owned atoms a little: the forward exchange must refresh ghosts
@@ -150,10 +154,12 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world,cells,shifted,ghost_centers", [
-    (2, 4, False, False), (2, 4, True, False), (3, 5, False, False),
-    (2, 6, True, True), (3, 9, False, True)])
-def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted, ghost_centers):
+@pytest.mark.parametrize("world,cells,shifted,ghost_centers,overlap", [
+    (2, 4, False, False, False), (2, 4, True, False, False), (3, 5, False, False, False),
+    (2, 6, True, True, False), (3, 9, False, True, False),
+    (2, 5, True, False, True), (2, 6, True, True, True)])
+def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted, ghost_centers,
+                                          overlap):
     """Classic mode (reverse force exchange) and ghost-centre mode (layer-1
     ghosts act as centres, no reverse exchange) both give the single-process
     energy, forces and virial."""
@@ -161,8 +167,8 @@ def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifte
     c = _case(cells)
     shift = np.array([0.03, -0.02, 0.01]) if shifted else None
     out = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out, ghost_centers), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out, ghost_centers, overlap),
+             nprocs=world, join=True)
     res = np.load(out)
     op = parse_param_text(c.params_text)
     off, nb = oracle.build_neighbor_list(c.xyz, c.box, c.periodic, op.r_cut_max, c.skin)
@@ -185,7 +191,7 @@ def test_slab_geometry_guards():
         [3, 0, 0, 1, 3, 0]
 
 
-def _nve_worker(rank, world, port, steps, out_path, nx=5, ghost_centers=False):
+def _nve_worker(rank, world, port, steps, out_path, nx=5, ghost_centers=False, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -198,10 +204,10 @@ def _nve_worker(rank, world, port, steps, out_path, nx=5, ghost_centers=False):
         halo = 3.2 + c.skin
         gid = partition(c.xyz, c.box, world, rank, halo)
         dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo,
-                            ghost_centers=ghost_centers)
+                            ghost_centers=ghost_centers, overlap=overlap)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
         nve = SlabNVE(dec, [28.0855], 3.2, c.skin)
-        nve.set_velocities(s.velocities[dec.gid])
+        nve.set_velocities(s.velocities[dec.gid])   # dec.gid: this rank's storage order
         samples = nve.run(steps, dt=0.001, thermo_every=10)
         g, x, v = nve.owned_state()
         parts = [None] * world
@@ -226,8 +232,9 @@ def _nve_case(nx=5):
                         0.5, systems.si_text(tb))
 
 
-@pytest.mark.parametrize("world,nx,ghost_centers", [(2, 5, False), (3, 5, False), (2, 6, True)])
-def test_slab_nve_matches_single_domain(tmp_path, world, nx, ghost_centers):
+@pytest.mark.parametrize("world,nx,ghost_centers,overlap", [
+    (2, 5, False, False), (3, 5, False, False), (2, 6, True, False), (2, 6, True, True)])
+def test_slab_nve_matches_single_domain(tmp_path, world, nx, ghost_centers, overlap):
     """SlabNVE (kick/drift of owned atoms, ghost exchange, rebuild vote,
     migration at rebuilds) on a hot 160-atom lattice over 2 and 3 gloo ranks
     follows the single-domain run of the same driver: atoms cross slab faces
@@ -237,8 +244,8 @@ def test_slab_nve_matches_single_domain(tmp_path, world, nx, ghost_centers):
     res = {}
     for w in (1, world):
         out = str(tmp_path / f"nve{w}.npz")
-        mp.spawn(_nve_worker, args=(w, _free_port(), steps, out, nx, ghost_centers), nprocs=w,
-                 join=True)
+        mp.spawn(_nve_worker, args=(w, _free_port(), steps, out, nx, ghost_centers, overlap),
+                 nprocs=w, join=True)
         res[w] = np.load(out)
     a, b = res[1], res[world]
     assert int(a["rebuilds"]) >= 2 and int(b["rebuilds"]) == int(a["rebuilds"])
