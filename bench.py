@@ -285,6 +285,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    # the multi-GPU code path (GpuEngine + Decomposition) on one rank: a smoke
+    # test of bench's N>1 branch where only one GPU is available
+    ap.add_argument("--decompose", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -307,7 +310,8 @@ def main():
     n = len(xyz)
     params = tb.parse_params(text)
     skin = 1.0
-    if world == 1:
+    use_dec = world > 1 or args.decompose
+    if not use_dec:
         ctx = tb.Context(params, local)
         ctx.set_system(xyz, species, box, per)
         ctx.build_neighbor_list(params.r_cut_max, skin)
@@ -393,7 +397,7 @@ def main():
 
     # e2e through the drop-in C-ABI call with host buffers
     e2e = None
-    if not args.no_e2e and world > 1:
+    if not args.no_e2e and use_dec:
         # per rank: owned positions in from pinned host memory, decomposed
         # evaluation (ghost exchange both ways), owned forces back to the host
         hx = torch.from_numpy(xyz[dec.gid].copy()).pin_memory()
@@ -417,9 +421,10 @@ def main():
         e1.record(stream)
         e1.synchronize()
         te = e0.elapsed_time(e1) / 1e3
-        tt = torch.tensor([te], device=f"cuda:{local}")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        te = float(tt.item())
+        if world > 1:
+            tt = torch.tensor([te], device=f"cuda:{local}")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
         e2e = {"value": n * args.steps / te, "unit": UNIT,
                "h2d_bytes_per_step": int(24 * n), "d2h_bytes_per_step": int(24 * n),
                "ms_per_step": 1e3 * te / args.steps,
