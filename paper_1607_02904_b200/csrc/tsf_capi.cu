@@ -55,6 +55,7 @@ template struct DevBuf<double4>;
 template struct DevBuf<int>;
 template struct DevBuf<unsigned char>;
 template struct DevBuf<unsigned long long>;
+template struct DevBuf<unsigned>;
 template struct DevBuf<Row<double>>;
 template struct DevBuf<Row<float>>;
 
@@ -176,6 +177,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     TSF_CUDA(cudaMemsetAsync(c.vel.get(), 0, 3 * nn * sizeof(double), c.stream));
   }
   if (geometry_changed) {
+    c.near_ok = false;
     c.skin_list.valid = false;
     c.short_list.valid = false;
     c.tiled = false;
@@ -473,7 +475,7 @@ int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
     c.device = device;
     TSF_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = c.stream;
-    c.flags.reserve(16);
+    c.flags.reserve(24);
     c.result.reserve(8);
     TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 16 * sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.result.get(), 0, 8 * sizeof(double), c.stream));

@@ -81,6 +81,20 @@ struct Ctx {
   DevBuf<float4> posf;         // [n] slot order float shadow for the cutoff pre-tests
   BoxF boxf{};
   DevBuf<double4> pos_ref;     // positions at the last list build (needs_rebuild)
+  // Near lists (k_filter): our own list builds also keep, per atom, the skin
+  // entries that lay within near_cut[q] = r_cut_max + h_q at the build
+  // (h_0 = s/4, h_1 = s/2, s the list's reach past every cutoff), in skin
+  // order.  Every position writer keeps the largest squared displacement since
+  // the build in flags[10]; while 2 |d|max < h_q an entry outside near list q
+  // is provably outside every cutoff, so the filter reads the smallest near
+  // list still valid instead of the skin list (crystalline Si: 4 entries
+  // instead of 16).  near_ok: pos_ref and the near lists describe the current
+  // slots (our build, not an external list).
+  ListState near_list[2];
+  double near_cut[2] = {0, 0};  // 0: no near lists
+  float near_t[2] = {0, 0};     // list q valid while |d|max^2 < near_t[q] = ((h_q - mu) / 2)^2
+  int near_pre[2] = {4, 4};     // ELL4 blocks the filter requests up front from list q
+  bool near_ok = false;
   DevBuf<double> xyz_stage;    // AoS staging for H2D / D2H, user order
   DevBuf<double> forces;       // [n][3] slot order (accumulation, MD)
   DevBuf<double> forces_user;  // [n][3] user order (download)
@@ -113,7 +127,10 @@ struct Ctx {
                                // skin count, both read synchronously in their own calls),
                                // [3] largest skin count, [4] largest short count,
                                // [5] |coord| max bits, [6] max cell occupancy,
-                               // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries
+                               // [7] species error, [8]/[9] atoms with > 4 / > 8 short entries,
+                               // [10] squared displacement max since the list build (float bits),
+                               // [11..16] atoms with > 4 / > 8 / > 12 entries in near list
+                               // 0 / 1 (list build)
   DevBuf<int> overflow;        // [3n] tier queues (G = 8, 16, 32 inputs)
 
   // slot range and position of the current compute() call in a two-phase

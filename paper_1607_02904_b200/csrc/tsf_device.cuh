@@ -90,6 +90,21 @@ __device__ __forceinline__ void track_coord_max(int* cmax, const double4& p) {
   if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(cmax, v);
 }
 
+// Largest squared displacement of a slot from its position at the last list
+// build (float bits rounded up, atomicMax; Ctx::near_list).  ref == nullptr: no list
+// of ours to track.  A NaN position propagates (its bits exceed +inf's), which
+// disables the filter's near-list path.
+__device__ __forceinline__ void track_disp(int* dmax, const double4* __restrict__ ref, int s,
+                                           const double4& p, const Box& box) {
+  if (!ref) return;
+  double dx, dy, dz;
+  displacement(ref[s], p, box, dx, dy, dz);
+  const float d2 = __double2float_ru(norm_sq_exact(dx, dy, dz));
+  const unsigned act = __activemask();
+  const int v = __reduce_max_sync(act, __float_as_int(d2));
+  if ((threadIdx.x & 31) == __ffs(act) - 1 && v > 0) atomicMax(dmax, v);
+}
+
 // [lo, hi] around cut^2: outside it the float r^2 decides the cutoff test
 // exactly as FP64 would.  Error model: each float coordinate is off by <=
 // |x| 2^-24, the float displacement (with a float box wrap) by ed <=
@@ -130,8 +145,7 @@ __device__ __forceinline__ WrapF wrap_of(const BoxF& box) {
   return w;
 }
 
-__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const WrapF& w,
-                                         float lo, float hi) {
+__device__ __forceinline__ float dist2f(const float4& a, const float4& b, const WrapF& w) {
   float d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
   // float minimum image d - L rint(d / L) (3 instructions per axis).  It can
   // pick the other image than the exact test only at |d| ~ L/2, where both
@@ -139,7 +153,12 @@ __device__ __forceinline__ int prefilter(const float4& a, const float4& b, const
   // such a pair takes the exact FP64 test.
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) d[ax] = fmaf(-w.l[ax], rintf(d[ax] * w.inv[ax]), d[ax]);
-  const float r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+  return d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+}
+
+__device__ __forceinline__ int prefilter(const float4& a, const float4& b, const WrapF& w,
+                                         float lo, float hi) {
+  const float r2 = dist2f(a, b, w);
   return r2 < lo ? kIn : (r2 > hi ? kOut : kUnsure);
 }
 

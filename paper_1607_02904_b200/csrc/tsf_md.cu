@@ -10,6 +10,10 @@ namespace {
 
 int blocks_for(std::int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
 
+// the reference positions position writers track displacements against
+// (Ctx::near_list), or nullptr when no list of ours describes the slots
+const double4* disp_ref(const Ctx& c) { return c.near_ok ? c.pos_ref.get() : nullptr; }
+
 // slot s holds user atom perm[s] (perm == nullptr: identity)
 __device__ __forceinline__ int user_of(const int* __restrict__ perm, int s) {
   return perm ? perm[s] : s;
@@ -21,7 +25,8 @@ __device__ __forceinline__ float4 shadow(const double4& p) {
 
 __global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ species,
                        const int* __restrict__ perm, int n, double4* __restrict__ pos,
-                       float4* __restrict__ posf, int* __restrict__ cmax) {
+                       float4* __restrict__ posf, int* __restrict__ cmax,
+                       const double4* __restrict__ dref, Box box) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int u = user_of(perm, s);
@@ -29,15 +34,18 @@ __global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ s
   pos[s] = p;
   posf[s] = shadow(p);
   track_coord_max(cmax, p);
+  track_disp(cmax + 5, dref, s, p, box);
 }
 
 __global__ void k_refresh_shadow(const double4* __restrict__ pos, int n,
-                                 float4* __restrict__ posf, int* __restrict__ cmax) {
+                                 float4* __restrict__ posf, int* __restrict__ cmax,
+                                 const double4* __restrict__ dref, Box box) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const double4 p = pos[s];
   posf[s] = shadow(p);
   track_coord_max(cmax, p);
+  track_disp(cmax + 5, dref, s, p, box);
 }
 
 __global__ void k_unpack(const double4* __restrict__ pos, const int* __restrict__ perm, int n,
@@ -88,7 +96,8 @@ __global__ void k_gather_pos(const double4* __restrict__ pos, const int* __restr
 __global__ void k_scatter_pos(double4* __restrict__ pos, float4* __restrict__ posf,
                               int* __restrict__ cmax, const int* __restrict__ inv,
                               const int* __restrict__ species, int lo, int m,
-                              const double* __restrict__ in) {
+                              const double* __restrict__ in, const double4* __restrict__ dref,
+                              Box box) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= m) return;
   const int s = slot_of(inv, lo + q);
@@ -96,6 +105,7 @@ __global__ void k_scatter_pos(double4* __restrict__ pos, float4* __restrict__ po
   pos[s] = p;
   posf[s] = shadow(p);
   track_coord_max(cmax, p);
+  track_disp(cmax + 5, dref, s, p, box);
 }
 
 __global__ void k_gather_f(const double* __restrict__ f, const int* __restrict__ inv, int lo,
@@ -136,7 +146,7 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        double dt, int drift, int kicks, Box box,
                        const double4* __restrict__ ref, double limit_sq,
                        int* __restrict__ moved_flag, const int* __restrict__ perm,
-                       int center_limit) {
+                       int center_limit, const double4* __restrict__ dref) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   // a decomposition's ghost copies are integrated by their owners and
@@ -169,12 +179,17 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
     pos[a] = p;
     posf[a] = shadow(p);
     track_coord_max(cmax, p);
-    if (moved_flag) {   // needs_rebuild (neighbor.cpp:134-141) on the new position
+    if (moved_flag || dref) {   // needs_rebuild (neighbor.cpp:134-141) on the new position
       double dx, dy, dz;
       displacement(ref[a], p, box, dx, dy, dz);
-      const bool moved = norm_sq_exact(dx, dy, dz) > limit_sq;
+      const double d2 = norm_sq_exact(dx, dy, dz);
       const unsigned act = __activemask();
-      if (__any_sync(act, moved) && (threadIdx.x & 31) == __ffs(act) - 1) atomicOr(moved_flag, 1);
+      if (moved_flag && __any_sync(act, d2 > limit_sq) && (threadIdx.x & 31) == __ffs(act) - 1)
+        atomicOr(moved_flag, 1);
+      if (dref) {   // track_disp on the displacement just computed
+        const int v = __reduce_max_sync(act, __float_as_int(__double2float_ru(d2)));
+        if ((threadIdx.x & 31) == __ffs(act) - 1 && v > 0) atomicMax(cmax + 5, v);
+      }
     }
   }
 }
@@ -270,7 +285,8 @@ void scatter_positions(Ctx& c, std::int64_t lo, std::int64_t m, const double* d_
   if (m <= 0) return;
   k_scatter_pos<<<blocks_for(m), kBlock, 0, c.stream>>>(c.pos.get(), c.posf.get(),
                                                         c.flags.get() + 5, inv_of(c),
-                                                        c.species.get(), int(lo), int(m), d_xyz);
+                                                        c.species.get(), int(lo), int(m), d_xyz,
+                                                        disp_ref(c), c.box);
   ++c.launches;
   c.forces_current = false;
 }
@@ -292,14 +308,16 @@ void pack_positions(Ctx& c) {
   if (c.n == 0) return;
   k_pack<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.xyz_stage.get(), c.species.get(),
                                                    perm_of(c), int(c.n), c.pos.get(),
-                                                   c.posf.get(), c.flags.get() + 5);
+                                                   c.posf.get(), c.flags.get() + 5, disp_ref(c),
+                                                   c.box);
   ++c.launches;
 }
 
 void refresh_shadow(Ctx& c) {
   if (c.n == 0) return;
   k_refresh_shadow<<<blocks_for(c.n), kBlock, 0, c.stream>>>(c.pos.get(), int(c.n),
-                                                             c.posf.get(), c.flags.get() + 5);
+                                                             c.posf.get(), c.flags.get() + 5,
+                                                             disp_ref(c), c.box);
   ++c.launches;
 }
 
@@ -333,6 +351,7 @@ void unpack_velocities(Ctx& c) {
 }
 
 void unsort(Ctx& c) {
+  c.near_ok = false;   // slots change: the near list no longer describes them
   if (!c.sorted || c.n == 0) {
     c.sorted = false;
     return;
@@ -367,7 +386,8 @@ void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
   k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
       c.pos.get(), c.posf.get(), c.flags.get() + 5, c.vel.get(), c.forces.get(), int(c.n),
       masses_of(c), dt, drift ? 1 : 0, kicks, c.box, c.pos_ref.get(), 0.25 * c.skin * c.skin,
-      check ? c.flags.get() + 2 : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c));
+      check ? c.flags.get() + 2 : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c),
+      disp_ref(c));
   ++c.launches;
 }
 

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -135,6 +136,23 @@ struct ListArgs {
   int ncls;          // slot classes (1, or 2 with an interior split)
 };
 
+// near-list outputs of a build (Ctx::near_list); nbr[0] == nullptr: none
+struct NearOut {
+  int* nbr[2];
+  int* cnt[2];
+  int* hist;         // [6]: atoms with > 4 / 8 / 12 entries in list 0, then list 1
+  double cut[2];
+};
+
+// near-list inputs of the filter (Ctx::near_list); nbr[0] == nullptr: none
+struct NearIn {
+  const int* nbr[2];
+  const int* cnt[2];
+  const int* dmax;   // squared displacement max since the build (float bits)
+  float t[2];
+  int pre[2];
+};
+
 // Skin list, one thread per slot: candidates are the stencil cells' slot
 // ranges (contiguous in the cell-sorted layout), tested on the float shadow
 // with the exact FP64 fallback inside the error band.
@@ -142,7 +160,8 @@ template <int CAP>
 __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, double bc2, int cap,
                                                       int* __restrict__ nbr,
                                                       int* __restrict__ cnt,
-                                                      int* __restrict__ max_count) {
+                                                      int* __restrict__ max_count,
+                                                      NearOut near) {
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
   float lo, hi;
@@ -188,6 +207,28 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
   }
   for (int s = 0; s < m; ++s) nbr[ell_at(s, at, a.npad)] = buf[s];
   cnt[at] = m;
+  if (near.nbr[0]) {
+    // the near lists (Ctx::near_list): every entry not provably beyond
+    // near_cut[q] — a float r^2 above the band's upper edge means the exact
+    // FP64 r^2 is beyond near_cut[q]^2 too
+    float lo0, hi0, lo1, hi1;
+    band_for(near.cut[0], a.cmax, lo0, hi0);
+    band_for(near.cut[1], a.cmax, lo1, hi1);
+    int w0 = 0, w1 = 0;
+    for (int s = 0; s < m; ++s) {
+      const float r2 = dist2f(pfa, a.posf[buf[s]], wrap);
+      if (!(r2 > hi0)) near.nbr[0][ell_at(w0++, at, a.npad)] = buf[s];
+      if (!(r2 > hi1)) near.nbr[1][ell_at(w1++, at, a.npad)] = buf[s];
+    }
+    near.cnt[0][at] = w0;
+    near.cnt[1][at] = w1;
+    const unsigned act = __activemask();
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int c = __popc(__ballot_sync(act, (q < 3 ? w0 : w1) > 4 * (q % 3 + 1)));
+      if ((threadIdx.x & 31) == __ffs(act) - 1 && c) atomicAdd(near.hist + q, c);
+    }
+  }
 }
 
 // Short list, one thread per slot: skin entries that pass their pair's bound,
@@ -272,12 +313,59 @@ __device__ __forceinline__ void keep_block(int* out, int at, int npad, int4 e, i
   if (bits & 8) out[ell_at(w++, at, npad)] = e.w;
 }
 
+// Filter the first m entries of list L for slot `at` into `out`; the first
+// `pre` ELL4 blocks (4 pre entries, pre <= 4, grid-uniform) are requested up
+// front.
+template <bool MULTI>
+__device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands& fb, int at,
+                                           const int* __restrict__ L, int m, int pre,
+                                           int* __restrict__ out) {
+  const float4 pfa = a.posf[at];
+  const int si = MULTI ? min(max(int(pfa.w), 0), fb.ns - 1) : 0;
+  int4 e[4];
+  // streamed once per step: evict-first keeps the gathered shadow in L2.
+  // Loaded without waiting for the count (every list has >= 16 allocated
+  // entries; those past the count are masked off in test_block), so count
+  // and list cost one DRAM round trip, not two.
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (b < pre) e[b] = __ldcs(reinterpret_cast<const int4*>(L + ell_at(4 * b, at, a.npad)));
+  // test all of them before any store or exact fallback: nothing between the
+  // gathers keeps the compiler from issuing them back to back
+  unsigned keep = 0, uns = 0;
+  unsigned long long prs = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (b < pre) {
+      int in, un, pr;
+      test_block<MULTI>(a, fb, at, pfa, si, e[b], m - 4 * b, in, un, pr);
+      keep |= unsigned(in) << (4 * b);
+      uns |= unsigned(un) << (4 * b);
+      if (MULTI) prs |= static_cast<unsigned long long>(unsigned(pr) & 0xffffu) << (16 * b);
+    }
+  }
+  if (uns) keep |= resolve_unsure<MULTI>(a, fb, L, at, 0, uns, prs);
+  int w = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (b < pre) keep_block(out, at, a.npad, e[b], int(keep >> (4 * b)) & 15, w);
+  for (int s0 = 4 * pre; s0 < m; s0 += 4) {
+    const int4 q = __ldcs(reinterpret_cast<const int4*>(L + ell_at(s0, at, a.npad)));
+    int in, un, pr;
+    test_block<MULTI>(a, fb, at, pfa, si, q, m - s0, in, un, pr);
+    unsigned k = unsigned(in);
+    if (un) k |= resolve_unsure<MULTI>(a, fb, L, at, s0, unsigned(un), unsigned(pr));
+    keep_block(out, at, a.npad, q, int(k), w);
+  }
+  return w;
+}
+
 template <bool MULTI>
 __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
     int* __restrict__ max_count, int* __restrict__ hist, void* __restrict__ zero_f,
-    int zero_bytes, int slot_lo, int slot_hi) {
+    int zero_bytes, int slot_lo, int slot_hi, NearIn near) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
   const int ns = pb.ns;
@@ -300,44 +388,25 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     float* z = static_cast<float*>(zero_f) + 3 * std::size_t(at);
     z[0] = z[1] = z[2] = 0.0f;
   }
-  const int m = skin_cnt[at];
+  // grid-uniform: the smallest near list no atom has moved far enough since
+  // the build to invalidate (Ctx::near_list), else the skin list
+  const int* L = skin;
+  const int* Lc = skin_cnt;
+  int pre = 4;
+  if (near.nbr[0]) {
+    const float d2 = __int_as_float(*near.dmax);
+    const int q = d2 < near.t[0] ? 0 : d2 < near.t[1] ? 1 : 2;
+    if (q < 2) {
+      L = near.nbr[q];
+      Lc = near.cnt[q];
+      pre = near.pre[q];
+    }
+  }
+  const int m = Lc[at];
   int w = 0;
   if (apply) {
     const FilterBands fb{slo, shi, sc2, ns, slo[0], shi[0], sc2[0], wrap_of(a.boxf)};
-    const float4 pfa = a.posf[at];
-    const int si = min(max(int(pfa.w), 0), ns - 1);
-    constexpr int kPre = 4;   // ELL4 blocks requested up front (16 entries)
-    int4 e[kPre];
-    // streamed once per step: evict-first keeps the gathered shadow in L2.
-    // Loaded without waiting for the count (every list has >= 16 allocated
-    // entries; those past the count are masked off in test_block), so count
-    // and list cost one DRAM round trip, not two.
-#pragma unroll
-    for (int b = 0; b < kPre; ++b)
-      e[b] = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(4 * b, at, a.npad)));
-    // test all 16 before any store or exact fallback: nothing between the
-    // gathers keeps the compiler from issuing them back to back
-    unsigned keep = 0, uns = 0;
-    unsigned long long prs = 0;
-#pragma unroll
-    for (int b = 0; b < kPre; ++b) {
-      int in, un, pr;
-      test_block<MULTI>(a, fb, at, pfa, si, e[b], m - 4 * b, in, un, pr);
-      keep |= unsigned(in) << (4 * b);
-      uns |= unsigned(un) << (4 * b);
-      if (MULTI) prs |= static_cast<unsigned long long>(unsigned(pr) & 0xffffu) << (16 * b);
-    }
-    if (uns) keep |= resolve_unsure<MULTI>(a, fb, skin, at, 0, uns, prs);
-#pragma unroll
-    for (int b = 0; b < kPre; ++b) keep_block(out, at, a.npad, e[b], int(keep >> (4 * b)) & 15, w);
-    for (int s0 = 4 * kPre; s0 < m; s0 += 4) {
-      const int4 q = __ldcs(reinterpret_cast<const int4*>(skin + ell_at(s0, at, a.npad)));
-      int in, un, pr;
-      test_block<MULTI>(a, fb, at, pfa, si, q, m - s0, in, un, pr);
-      unsigned k = unsigned(in);
-      if (un) k |= resolve_unsure<MULTI>(a, fb, skin, at, s0, unsigned(un), unsigned(pr));
-      keep_block(out, at, a.npad, q, int(k), w);
-    }
+    w = filter_list<MULTI>(a, fb, at, L, m, pre, out);
   } else {
     for (int s = 0; s < m; ++s) out[ell_at(s, at, a.npad)] = skin[ell_at(s, at, a.npad)];
     w = m;
@@ -424,7 +493,11 @@ template <int CAP>
 void launch_skin(Ctx& c, double bc2, int cap) {
   k_skin_list<CAP><<<blocks_for(c.n), kBlock, 0, c.stream>>>(
       list_args(c), std::sqrt(bc2), bc2, cap, c.skin_list.nbr.get(), c.skin_list.cnt.get(),
-      c.flags.get() + 3);
+      c.flags.get() + 3,
+      NearOut{{c.near_cut[0] > 0 ? c.near_list[0].nbr.get() : nullptr, c.near_list[1].nbr.get()},
+              {c.near_list[0].cnt.get(), c.near_list[1].cnt.get()},
+              c.flags.get() + 11,
+              {c.near_cut[0], c.near_cut[1]}});
   ++c.launches;
 }
 
@@ -451,6 +524,24 @@ void list_build(Ctx& c, double cutoff, double skin) {
   c.cutoff = cutoff;
   c.skin = skin;
   const int n = int(c.n);
+  // near list (Ctx::near_list): entries within r_cut_max + h, h = s/2, s the
+  // list's reach past every cutoff; usable while 2 |d|max + mu < h, mu
+  // absorbing the FP64 rounding of the displacements that test relies on
+  c.near_ok = false;
+  c.near_cut[0] = c.near_cut[1] = 0.0;
+  const char* near_env = std::getenv("TSF_NEAR");   // TSF_NEAR=0: off (A/B runs)
+  if (c.has_potential && !(near_env && near_env[0] == '0')) {
+    const double rf = c.params.r_cut_max();
+    const double mu = 1e-6 * std::max(1.0, rf);
+    if (bc - rf > 16.0 * mu) {
+      for (int q = 0; q < 2; ++q) {
+        const double h = 0.25 * (q + 1) * (bc - rf);
+        const double t = 0.5 * (h - mu);
+        c.near_cut[q] = rf + h;
+        c.near_t[q] = std::nextafter(float(t * t), 0.0f);
+      }
+    }
+  }
 
   // grid (neighbor.cpp:50-77)
   double lo[3] = {0, 0, 0}, hi[3] = {c.box.len[0], c.box.len[1], c.box.len[2]};
@@ -542,6 +633,13 @@ void list_build(Ctx& c, double cutoff, double skin) {
   for (int attempt = 0; attempt < 3; ++attempt) {
     c.skin_list.nbr.reserve(std::size_t(cap) * c.npad + 1);
     c.skin_list.cnt.reserve(std::size_t(c.npad) + 1);
+    if (c.near_cut[0] > 0.0) {
+      for (ListState& l : c.near_list) {
+        l.nbr.reserve(std::size_t(cap) * c.npad + 1);
+        l.cnt.reserve(std::size_t(c.npad) + 1);
+      }
+      TSF_CUDA(cudaMemsetAsync(c.flags.get() + 11, 0, 6 * sizeof(int), c.stream));
+    }
     TSF_CUDA(cudaMemsetAsync(c.skin_list.cnt.get(), 0, sizeof(int) * c.npad, c.stream));
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 3, 0, sizeof(int), c.stream));
     if (n > 0) {
@@ -550,14 +648,28 @@ void list_build(Ctx& c, double cutoff, double skin) {
       else if (cap <= 128) launch_skin<128>(c, bc2, cap);
       else launch_skin<512>(c, bc2, cap);
     }
-    int mx = 0;
-    TSF_CUDA(cudaMemcpyAsync(&mx, c.flags.get() + 3, sizeof(int), cudaMemcpyDeviceToHost,
-                             c.stream));
+    int f[17] = {0};
+    TSF_CUDA(cudaMemcpyAsync(f, c.flags.get(), sizeof f, cudaMemcpyDeviceToHost, c.stream));
     TSF_CUDA(cudaStreamSynchronize(c.stream));
+    const int mx = f[3];
     c.skin_list.max_count = mx;
     if (mx <= cap) {
       c.skin_list.cap = cap;
       c.skin_list.valid = true;
+      // the filter requests 4 near_pre entries of a near list up front: the
+      // fewest blocks that leave at most 1/256 of the atoms to the serial tail
+      const int tail = n / 256;
+      for (int q = 0; q < 2; ++q) {
+        c.near_list[q].cap = cap;
+        const int* o = f + 11 + 3 * q;
+        c.near_pre[q] = o[0] <= tail ? 1 : o[1] <= tail ? 2 : o[2] <= tail ? 3 : 4;
+      }
+      if (std::getenv("TSF_VERBOSE"))
+        std::fprintf(stderr,
+                     "tsf: list build n=%d skin max %d; near lists: over 4/8/12 %d %d %d, "
+                     "%d %d %d -> pre %d %d\n",
+                     n, mx, f[11], f[12], f[13], f[14], f[15], f[16], c.near_pre[0],
+                     c.near_pre[1]);
       break;
     }
     if (mx > 512)
@@ -566,6 +678,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
     cap = mx <= 32 ? 32 : mx <= 64 ? 64 : mx <= 128 ? 128 : 512;
   }
   snapshot_reference_positions(c);
+  c.near_ok = c.near_cut[0] > 0.0;
   c.short_max_stale = true;
   c.short_list.valid = false;
   ++c.list_version;
@@ -577,6 +690,7 @@ void snapshot_reference_positions(Ctx& c) {
   c.pos_ref.reserve(std::size_t(std::max<std::int64_t>(c.n, 1)));
   TSF_CUDA(cudaMemcpyAsync(c.pos_ref.get(), c.pos.get(), sizeof(double4) * c.n,
                            cudaMemcpyDeviceToDevice, c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 10, 0, sizeof(int), c.stream));
 }
 
 void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int lo, int hi) {
@@ -616,11 +730,18 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
     // (a TMA-staged, persistent variant measured slower: 0.138 vs 0.114 ms at
     // 2M atoms — its staging buffers take the L1 the position gathers hit,
     // 58% -> 9% hit rate)
+    NearIn near{};
+    if (c.near_ok && mode != FilterMode::Copy)
+      near = NearIn{{c.near_list[0].nbr.get(), c.near_list[1].nbr.get()},
+                    {c.near_list[0].cnt.get(), c.near_list[1].cnt.get()},
+                    c.flags.get() + 10,
+                    {c.near_t[0], c.near_t[1]},
+                    {c.near_pre[0], c.near_pre[1]}};
     (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(std::max(hi - lo, 1)), kBlock, 0,
                                                        c.stream>>>(
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
         c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
-        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi);
+        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi, near);
     ++c.launches;
   }
   s.valid = true;

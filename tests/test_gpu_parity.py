@@ -385,3 +385,48 @@ def test_graph_replay_follows_new_positions(tb, oracle):
     assert np.abs(f1 - ref["forces"]).max() <= F_TOL_D
     for c in (ctx, fresh):
         c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["crystal", "liquid", "sic"])
+def test_near_list_filter_is_exact(tb, kind, sic_text):
+    """While 2 |d|max < h (h = s/4, s/2) the filter reads a near list — the
+    skin entries within r_cut_max + h at the build — instead of the skin list
+    (Ctx::near_list in tsf_context.hpp).  Move every atom by exactly |d| = D
+    (random directions, so pairs approach by up to 2 D) on both sides of each
+    switch (D = s/8, s/4) and check the short list and forces against a
+    context fed the same skin list externally, which never uses a near list."""
+    if kind == "crystal":
+        case = systems.perturbed(tb, 4, 0.12, 32, skin=1.0)
+    elif kind == "liquid":
+        case = systems.liquid_like(tb, cells=4, skin=1.0)
+    else:
+        case = systems.zincblende(tb, sic_text, cells=4, jitter=0.1, seed=3, skin=1.0)
+    params, ctx = _ctx(tb, case)
+    skin_off, skin_nb = ctx.export_neighbors("skin")
+    fresh = tb.Context(params, 0)
+    rng = np.random.default_rng(11)
+    reach = case.skin         # list cutoff r_cut_max + skin: s = skin
+    for frac in (0.0, 0.05, 0.124, 0.126, 0.2, 0.249, 0.251, 0.3, 0.49):
+        d = rng.normal(size=case.xyz.shape)
+        d *= (frac * reach) / np.linalg.norm(d, axis=1, keepdims=True)
+        moved = np.mod(case.xyz + d, case.box)
+        ctx.set_positions(moved)
+        assert not ctx.needs_rebuild()
+        fresh.set_system(moved, case.species, case.box, case.periodic)
+        fresh.set_neighbor_list(skin_off, skin_nb, params.r_cut_max, case.skin)
+        for which in ("short",):
+            a_off, a_nb = ctx.export_neighbors(which)
+            b_off, b_nb = fresh.export_neighbors(which)
+            assert np.array_equal(a_off, b_off) and np.array_equal(a_nb, b_nb), frac
+        for prec in ("double", "mixed"):
+            e1, f1, _ = ctx.compute(prec, deterministic=True)
+            e2, f2, _ = fresh.compute(prec, deterministic=True)
+            # same lists; the two contexts differ only in slot order (summation
+            # order of the energy, and of float partials in mixed)
+            tol = 1e-13 if prec == "double" else 1e-6
+            assert abs(e1 - e2) <= tol * abs(e2), (frac, prec)
+            ftol = 1e-12 if prec == "double" else 2e-6 * max(1.0, np.abs(f2).max())
+            assert np.abs(f1 - f2).max() <= ftol, (frac, prec)
+    for c in (ctx, fresh):
+        c.close()
