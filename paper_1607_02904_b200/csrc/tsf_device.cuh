@@ -81,13 +81,21 @@ struct BoxF {
 
 enum : int { kOut = 0, kIn = 1, kUnsure = 2 };
 
+// atomicMax(p, v) by one lane, skipped when p already holds >= v: the
+// tracked maxima only grow between resets (which are stream-ordered before
+// the kernel), so a stale read can only cost a redundant atomic — and
+// same-address atomics from every warp of a 2M-atom pass serialise in L2.
+__device__ __forceinline__ void lane_max(int* p, int v) {
+  if (v > __ldcg(p)) atomicMax(p, v);
+}
+
 // Largest |coordinate| ever packed into the shadow (float bits, atomicMax);
 // the pre-test bands are derived from it in-kernel, so no host round trip.
 __device__ __forceinline__ void track_coord_max(int* cmax, const double4& p) {
   const float m = __double2float_ru(fmax(fabs(p.x), fmax(fabs(p.y), fabs(p.z))));
   const unsigned act = __activemask();
   const int v = __reduce_max_sync(act, __float_as_int(m));
-  if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(cmax, v);
+  if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(cmax, v);
 }
 
 // Largest squared displacement of a slot from its position at the last list
@@ -102,7 +110,7 @@ __device__ __forceinline__ void track_disp(int* dmax, const double4* __restrict_
   const float d2 = __double2float_ru(norm_sq_exact(dx, dy, dz));
   const unsigned act = __activemask();
   const int v = __reduce_max_sync(act, __float_as_int(d2));
-  if ((threadIdx.x & 31) == __ffs(act) - 1 && v > 0) atomicMax(dmax, v);
+  if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(dmax, v);
 }
 
 // [lo, hi] around cut^2: outside it the float r^2 decides the cutoff test

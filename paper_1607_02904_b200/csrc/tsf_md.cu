@@ -188,7 +188,7 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
         atomicOr(moved_flag, 1);
       if (dref) {   // track_disp on the displacement just computed
         const int v = __reduce_max_sync(act, __float_as_int(__double2float_ru(d2)));
-        if ((threadIdx.x & 31) == __ffs(act) - 1 && v > 0) atomicMax(cmax + 5, v);
+        if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(cmax + 5, v);
       }
     }
   }
