@@ -141,8 +141,14 @@ struct NearOut {
   int* nbr[2];
   int* cnt[2];
   int* hist;         // [6]: atoms with > 4 / 8 / 12 entries in list 0, then list 1
-  double cut[2];
+  double cut[2];     // r_cut_max + h_q
+  double h[2];
 };
+
+// Near-list entries carry a "sure" bit: the pair lay within its species
+// pair's filter bound minus h_q at the build, so while the list is valid
+// (2 |d|max < h_q) it is inside that bound — kept without a gather.
+constexpr unsigned kSure = 0x80000000u;
 
 // near-list inputs of the filter (Ctx::near_list); nbr[0] == nullptr: none
 struct NearIn {
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
                                                       int* __restrict__ nbr,
                                                       int* __restrict__ cnt,
                                                       int* __restrict__ max_count,
-                                                      NearOut near) {
+                                                      NearOut near, PairBounds pb) {
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
   float lo, hi;
@@ -214,11 +220,19 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
     float lo0, hi0, lo1, hi1;
     band_for(near.cut[0], a.cmax, lo0, hi0);
     band_for(near.cut[1], a.cmax, lo1, hi1);
+    const int si = min(max(int(pfa.w), 0), pb.ns - 1);
     int w0 = 0, w1 = 0;
     for (int s = 0; s < m; ++s) {
-      const float r2 = dist2f(pfa, a.posf[buf[s]], wrap);
-      if (!(r2 > hi0)) near.nbr[0][ell_at(w0++, at, a.npad)] = buf[s];
-      if (!(r2 > hi1)) near.nbr[1][ell_at(w1++, at, a.npad)] = buf[s];
+      const float4 pfb = a.posf[buf[s]];
+      const float r2 = dist2f(pfa, pfb, wrap);
+      const double cut = pb.cut[si * pb.ns + min(max(int(pfb.w), 0), pb.ns - 1)];
+      // sure: the float r^2 below the band's lower edge around (cut - h_q)^2
+      float slo0, shi0, slo1, shi1;
+      band_for(fmax(cut - near.h[0], 0.0), a.cmax, slo0, shi0);
+      band_for(fmax(cut - near.h[1], 0.0), a.cmax, slo1, shi1);
+      const unsigned b = unsigned(buf[s]);
+      if (!(r2 > hi0)) near.nbr[0][ell_at(w0++, at, a.npad)] = int(b | (r2 < slo0 ? kSure : 0u));
+      if (!(r2 > hi1)) near.nbr[1][ell_at(w1++, at, a.npad)] = int(b | (r2 < slo1 ? kSure : 0u));
     }
     near.cnt[0][at] = w0;
     near.cnt[1][at] = w1;
@@ -260,10 +274,18 @@ struct FilterBands {
 // holds the species-pair index of each entry (MULTI), 4 bits each.
 template <bool MULTI>
 __device__ __forceinline__ void test_block(const ListArgs& a, const FilterBands& fb, int at,
-                                           const float4& pfa, int si, int4 e, int valid,
+                                           const float4& pfa, int si, int4& e, int valid,
                                            int& in, int& unsure, int& prs) {
-  const int bb[4] = {valid > 0 ? e.x : at, valid > 1 ? e.y : at, valid > 2 ? e.z : at,
-                     valid > 3 ? e.w : at};
+  // sure entries (near lists, kSure) are kept without a gather; the bit is
+  // stripped here so the entries written out are plain slots
+  const int sure = int((unsigned(e.x) >> 31) | ((unsigned(e.y) >> 30) & 2u) |
+                       ((unsigned(e.z) >> 29) & 4u) | ((unsigned(e.w) >> 28) & 8u));
+  e.x &= 0x7fffffff;
+  e.y &= 0x7fffffff;
+  e.z &= 0x7fffffff;
+  e.w &= 0x7fffffff;
+  const int bb[4] = {valid > 0 && !(sure & 1) ? e.x : at, valid > 1 && !(sure & 2) ? e.y : at,
+                     valid > 2 && !(sure & 4) ? e.z : at, valid > 3 && !(sure & 8) ? e.w : at};
   float4 pf[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) pf[u] = a.posf[bb[u]];
@@ -284,8 +306,8 @@ __device__ __forceinline__ void test_block(const ListArgs& a, const FilterBands&
     unsure |= (v == kUnsure) << u;
   }
   const int vm = (1 << max(0, min(valid, 4))) - 1;
-  in &= vm;
-  unsure &= vm;
+  in = (in | sure) & vm;
+  unsure &= vm & ~sure;
 }
 
 // Rare: entries inside the float error band take the exact FP64 test (the
@@ -298,7 +320,7 @@ __device__ __forceinline__ unsigned resolve_unsure(const ListArgs& a, const Filt
   while (unsure) {
     const int q = __ffs(unsure) - 1;
     unsure &= unsure - 1;
-    const int b = skin[ell_at(s_base + q, at, a.npad)];
+    const int b = skin[ell_at(s_base + q, at, a.npad)] & 0x7fffffff;
     const double c2 = MULTI ? fb.c2[(prs >> (4 * q)) & 15] : fb.c20;
     if (exact_within(a.pos, at, b, a.box, c2)) in |= 1u << q;
   }
@@ -350,7 +372,7 @@ __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands&
   for (int b = 0; b < 4; ++b)
     if (b < pre) keep_block(out, at, a.npad, e[b], int(keep >> (4 * b)) & 15, w);
   for (int s0 = 4 * pre; s0 < m; s0 += 4) {
-    const int4 q = __ldcs(reinterpret_cast<const int4*>(L + ell_at(s0, at, a.npad)));
+    int4 q = __ldcs(reinterpret_cast<const int4*>(L + ell_at(s0, at, a.npad)));
     int in, un, pr;
     test_block<MULTI>(a, fb, at, pfa, si, q, m - s0, in, un, pr);
     unsigned k = unsigned(in);
@@ -489,15 +511,48 @@ ListArgs list_args(Ctx& c) {
   return a;
 }
 
+// The filter's bound per (species of i, species of k) for a mode: the
+// reference's r_cut_max (exports), or the largest cutsq of any row (i, *, k)
+// (the force path, PairBounds).
+PairBounds pair_bounds(const Ctx& c, FilterMode mode) {
+  PairBounds pb{};
+  if (mode != FilterMode::Copy) {
+    const int ns = c.params.species_count();
+    pb.ns = ns;
+    const double rc = c.params.r_cut_max();
+    for (int i = 0; i < ns; ++i)
+      for (int k = 0; k < ns; ++k) {
+        double c2 = rc * rc, cut = rc;   // the reference's test (neighbor.cpp:146)
+        if (mode == FilterMode::Pair) {
+          c2 = 0;
+          for (int j = 0; j < ns; ++j) {
+            const double cc = c.params.entry(i, j, k).cutoff();
+            c2 = std::max(c2, cc * cc);   // the force kernel's cutsq values
+          }
+          cut = std::sqrt(c2);
+        }
+        pb.c2[i * ns + k] = c2;
+        pb.cut[i * ns + k] = cut;
+      }
+  } else {
+    pb.ns = 1;
+  }
+  return pb;
+}
+
 template <int CAP>
 void launch_skin(Ctx& c, double bc2, int cap) {
+  const bool near = c.near_cut[0] > 0.0;
+  const double rf = near ? c.params.r_cut_max() : 0.0;
   k_skin_list<CAP><<<blocks_for(c.n), kBlock, 0, c.stream>>>(
       list_args(c), std::sqrt(bc2), bc2, cap, c.skin_list.nbr.get(), c.skin_list.cnt.get(),
       c.flags.get() + 3,
-      NearOut{{c.near_cut[0] > 0 ? c.near_list[0].nbr.get() : nullptr, c.near_list[1].nbr.get()},
+      NearOut{{near ? c.near_list[0].nbr.get() : nullptr, c.near_list[1].nbr.get()},
               {c.near_list[0].cnt.get(), c.near_list[1].cnt.get()},
               c.flags.get() + 11,
-              {c.near_cut[0], c.near_cut[1]}});
+              {c.near_cut[0], c.near_cut[1]},
+              {c.near_cut[0] - rf, c.near_cut[1] - rf}},
+      near ? pair_bounds(c, FilterMode::Pair) : PairBounds{{}, {}, 1});
   ++c.launches;
 }
 
@@ -704,28 +759,7 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 4, 0, sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 8, 0, 2 * sizeof(int), c.stream));
   }
-  PairBounds pb{};
-  if (mode != FilterMode::Copy) {
-    const int ns = c.params.species_count();
-    pb.ns = ns;
-    const double rc = c.params.r_cut_max();
-    for (int i = 0; i < ns; ++i)
-      for (int k = 0; k < ns; ++k) {
-        double c2 = rc * rc, cut = rc;   // the reference's test (neighbor.cpp:146)
-        if (mode == FilterMode::Pair) {
-          c2 = 0;
-          for (int j = 0; j < ns; ++j) {
-            const double cc = c.params.entry(i, j, k).cutoff();
-            c2 = std::max(c2, cc * cc);   // the force kernel's cutsq values
-          }
-          cut = std::sqrt(c2);
-        }
-        pb.c2[i * ns + k] = c2;
-        pb.cut[i * ns + k] = cut;
-      }
-  } else {
-    pb.ns = 1;
-  }
+  const PairBounds pb = pair_bounds(c, mode);
   if (c.n > 0) {
     // (a TMA-staged, persistent variant measured slower: 0.138 vs 0.114 ms at
     // 2M atoms — its staging buffers take the L1 the position gathers hit,
