@@ -35,6 +35,14 @@ def fold(path):
         d = dict(zip(h, r))
         name = d["Kernel Name"]
         kind = "filter" if "k_filter" in name else "force"
+        if kind == "force":
+            # <R, Acc, G, SPEC, DET, OVF, FOREIGN>: only the main launch
+            # (OVF = FOREIGN = 0), never a tier launch
+            lt = name.find("k_force<") + len("k_force<")
+            args = [x.strip() for x in name[lt:name.find(">", lt)].split(",")]
+            if len(args) >= 7 and (args[5] not in ("0", "(bool)0", "false")
+                                   or args[6] not in ("0", "(bool)0", "false")):
+                continue
         e = per.setdefault(d["ID"], {"kind": kind, "name": name})
         v = float(d["Metric Value"].replace(",", ""))
         unit = d["Metric Unit"]

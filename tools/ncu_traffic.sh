@@ -1,6 +1,6 @@
 # usage: bash tools/ncu_traffic.sh [config...]
 # DRAM bytes, duration and pipe utilisation per launch of the main force
-# kernel and the filter
+# kernel (OVF = FOREIGN = false: not the tier launches) and the filter
 # for each config x precision (tools/ncu_traffic.py folds the CSVs into
 # profiles/ncu_traffic.json for bench.py's roofline.traffic).  One GPU; each
 # bench command runs once without ncu first.
@@ -22,7 +22,7 @@ for C in $CFGS; do
     M=$M,sm__throughput.avg.pct_of_peak_sustained_elapsed
     ncu --metrics $M \
         --clock-control none --kernel-name-base demangled --nvtx --nvtx-include "bench_steps/" \
-        -k 'regex:k_force<.*\(bool\)0>|k_filter' -s 2 -c 4 --csv \
+        -k 'regex:k_force<.*\(bool\)0, \(bool\)0>|k_filter' -s 2 -c 4 --csv \
         --log-file gpurun_out/traffic/${C}_$P.csv $B > gpurun_out/traffic/ncu_${C}_$P.log 2>&1
     echo "ncu $C $P rc=$?"
   done
