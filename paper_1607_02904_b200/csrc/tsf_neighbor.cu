@@ -368,9 +368,19 @@ __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands&
   }
   if (uns) keep |= resolve_unsure<MULTI>(a, fb, L, at, 0, uns, prs);
   int w = 0;
+  const int nv = min(m, 4 * pre);
+  if (keep == (1u << nv) - 1u) {
+    // every entry kept (a crystal's near list: all sure): the blocks go out
+    // as loaded, one 16-byte store each (entries past the count are never read)
 #pragma unroll
-  for (int b = 0; b < 4; ++b)
-    if (b < pre) keep_block(out, at, a.npad, e[b], int(keep >> (4 * b)) & 15, w);
+    for (int b = 0; b < 4; ++b)
+      if (b < pre && 4 * b < nv) *reinterpret_cast<int4*>(out + ell_at(4 * b, at, a.npad)) = e[b];
+    w = nv;
+  } else {
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (b < pre) keep_block(out, at, a.npad, e[b], int(keep >> (4 * b)) & 15, w);
+  }
   for (int s0 = 4 * pre; s0 < m; s0 += 4) {
     int4 q = __ldcs(reinterpret_cast<const int4*>(L + ell_at(s0, at, a.npad)));
     int in, un, pr;
