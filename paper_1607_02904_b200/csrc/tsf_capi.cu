@@ -477,7 +477,7 @@ int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
     c.own_stream = c.stream;
     c.flags.reserve(24);
     c.result.reserve(8);
-    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 16 * sizeof(int), c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 24 * sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.result.get(), 0, 8 * sizeof(double), c.stream));
     tsf::upload_params(c);
     c.masses.assign(std::size_t(c.params.species_count()), 28.0855);
