@@ -274,11 +274,25 @@ void evaluate_launches(Ctx& c, tsf::Precision p, std::uint32_t flags) {
     }
   }
   tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair,
-                   zf, zb);
+                   zf, zb, 0, -1, true);
   c.mark(1);
-  tsf::compute(c, p, zf ? (flags | tsf::kFlagForcesZeroed) : flags);
+  tsf::compute(c, p, (zf ? (flags | tsf::kFlagForcesZeroed) : flags) | tsf::kFlagFlagsZeroed);
   c.mark(4);
 }
+
+}  // namespace (reopened below)
+
+namespace tsf {
+int pdl_level() {
+  static const int level = [] {
+    const char* e = std::getenv("TSF_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return level;
+}
+}  // namespace tsf
+
+namespace {
 
 bool graphs_enabled() {
   static const bool on = [] {

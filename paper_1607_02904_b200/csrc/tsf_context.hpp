@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "tsf_device.cuh"
@@ -31,6 +32,34 @@ struct CudaError : std::runtime_error {
 
 void check_cuda(cudaError_t e, const char* what);
 #define TSF_CUDA(call) ::tsf::check_cuda((call), #call)
+
+// Launch with programmatic stream serialization (see griddep_wait): the
+// kernel must begin with griddep_wait().
+// TSF_PDL=0: plain launches (A/B runs).  Only the force chain (main -> tiers
+// -> reduction) uses it: letting the main launch in behind the filter as well
+// made the 2M-atom mixed/single step 15% slower (its blocks take the filter's
+// last-wave slots), tools/ab.py.
+int pdl_level();
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t stream,
+                Args&&... args) {
+  if (pdl_level() == 0) {
+    kernel<<<grid, block, 0, stream>>>(std::forward<Args>(args)...);
+    TSF_CUDA(cudaGetLastError());
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TSF_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Per-step reduction slots (energy + 6 virial components) per block.
 constexpr int kRedWidth = 8;
@@ -178,8 +207,9 @@ enum class FilterMode { Copy = 0, Cutoff = 1, Pair = 2 };
 // zero_forces: optional [n][3] accumulator (zero_bytes = 8 double / 4 float)
 // the filter zeroes for the atomic-mode force kernel
 // lo / hi: the slot range (two-phase evaluation); hi < 0: all atoms
+// zero_flags: the filter launch also zeroes flags[0..3] (kFlagFlagsZeroed)
 void list_filter(Ctx& c, FilterMode mode, void* zero_forces = nullptr, int zero_bytes = 0,
-                 int lo = 0, int hi = -1);
+                 int lo = 0, int hi = -1, bool zero_flags = false);
 bool list_needs_rebuild(Ctx& c);
 void snapshot_reference_positions(Ctx& c);
 
@@ -188,6 +218,8 @@ enum class Precision { F64 = 0, Mixed = 1, F32 = 2 };
 // compute() flag (internal, above the public TSF_* bits): the atomic-mode
 // force accumulator was zeroed by the filter launch
 constexpr std::uint32_t kFlagForcesZeroed = 1u << 16;
+// the filter launch zeroed flags[0..3] (error bits and tier queue counts)
+constexpr std::uint32_t kFlagFlagsZeroed = 1u << 17;
 void compute(Ctx& c, Precision prec, std::uint32_t flags);
 void upload_params(Ctx& c);
 

@@ -81,6 +81,15 @@ struct BoxF {
 
 enum : int { kOut = 0, kIn = 1, kUnsure = 2 };
 
+// Programmatic dependent launch (launch_pdl): griddep_wait() returns once the
+// preceding grid in the stream has completed and its writes are visible — a
+// no-op for a kernel launched normally — so a kernel that starts with it keeps
+// stream semantics; griddep_launch() lets the next launch_pdl kernel be
+// scheduled (and sit in its own griddep_wait) while this one drains, which
+// hides the launch gap between the force chain's kernels.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // atomicMax(p, v) by one lane, skipped when p already holds >= v: the
 // tracked maxima only grow between resets (which are stream-ordered before
 // the kernel), so a stale read can only cost a redundant atomic — and

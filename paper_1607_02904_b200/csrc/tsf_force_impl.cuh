@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
   __shared__ double s_red[kBlock / 32][kRedWidth];
 
+  griddep_wait();     // launch_pdl: the previous launch has completed
+  griddep_launch();
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   Acc e_acc = 0;
@@ -569,6 +571,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
 __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partials, int nblocks,
                                                double* __restrict__ out) {
   __shared__ double s[256][7];
+  griddep_wait();
   const int t = threadIdx.x;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int b = t; b < nblocks; b += 256)
@@ -713,7 +716,7 @@ int launch_main(Ctx& c, ForceArgs<R> a) {
   auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN>;
   const int blocks = persistent_blocks(kern, tiles);
   c.mark(2);
-  kern<<<blocks, kBlock, 0, c.stream>>>(a);
+  launch_pdl(kern, blocks, kBlock, c.stream, a);
   c.mark(3);
   ++c.launches;
   return blocks;
@@ -770,7 +773,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     a.ovf_in_count = a.flags + 1 + cur;
     a.ovf_out = last ? nullptr : qbuf + std::size_t(cur + 1) * c.n;
     a.ovf_out_count = a.flags + 2 + cur;
-    kernel<<<blocks, kBlock, 0, c.stream>>>(a);
+    launch_pdl(kernel, blocks, kBlock, c.stream, a);
     nb += blocks;
     ++c.launches;
     if (!last) ++cur;
@@ -788,7 +791,8 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
       ++c.launches;
     }
   }
-  k_reduce<<<1, 256, 0, c.stream>>>(c.partials.get(), nb, c.result.get());
+  launch_pdl(k_reduce, 1, 256, c.stream, static_cast<const double*>(c.partials.get()), nb,
+             c.result.get());
   ++c.launches;
 }
 
@@ -835,7 +839,8 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   c.overflow.reserve(std::max<std::size_t>(3 * n, 1));
   c.partials.reserve(std::size_t(32 * 148 + 4 * kOverflowBlocks + 8) * kRedWidth);
   a.partials = c.partials.get();
-  if (c.phase_first) TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));
+  if (c.phase_first && !(flags & kFlagFlagsZeroed))
+    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));
 
   constexpr bool kF32 = std::is_same<Acc, float>::value;
   if (det) {

@@ -397,9 +397,11 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
     int* __restrict__ max_count, int* __restrict__ hist, void* __restrict__ zero_f,
-    int zero_bytes, int slot_lo, int slot_hi, NearIn near) {
+    int zero_bytes, int slot_lo, int slot_hi, NearIn near, int* __restrict__ zero_flags) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
+  // error bits and tier queue counts of the force launches that follow
+  if (zero_flags && blockIdx.x == 0 && threadIdx.x < 4) zero_flags[threadIdx.x] = 0;
   const int ns = pb.ns;
   if (apply && int(threadIdx.x) < ns * ns) {
     float lo, hi;
@@ -758,7 +760,8 @@ void snapshot_reference_positions(Ctx& c) {
   TSF_CUDA(cudaMemsetAsync(c.flags.get() + 10, 0, sizeof(int), c.stream));
 }
 
-void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int lo, int hi) {
+void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int lo, int hi,
+                 bool zero_flags) {
   if (hi < 0) hi = int(c.n);
   ListState& s = c.short_list;
   s.cap = c.skin_list.cap;
@@ -785,7 +788,8 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
                                                        c.stream>>>(
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
         c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
-        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi, near);
+        c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi, near,
+        zero_flags ? c.flags.get() : nullptr);
     ++c.launches;
   }
   s.valid = true;
