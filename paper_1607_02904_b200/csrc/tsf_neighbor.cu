@@ -145,9 +145,9 @@ struct NearOut {
   double h[2];
 };
 
-// Near-list entries carry a "sure" bit: the pair lay within its species
-// pair's filter bound minus h_q at the build, so while the list is valid
-// (2 |d|max < h_q) it is inside that bound — kept without a gather.
+// Near-list entries carry a "sure" bit: the pair lay within the smallest
+// filter bound of any species pair minus h_q at the build, so while the list
+// is valid (2 |d|max < h_q) it is inside every bound — kept without a gather.
 constexpr unsigned kSure = 0x80000000u;
 
 // near-list inputs of the filter (Ctx::near_list); nbr[0] == nullptr: none
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
                                                       int* __restrict__ nbr,
                                                       int* __restrict__ cnt,
                                                       int* __restrict__ max_count,
-                                                      NearOut near, PairBounds pb) {
+                                                      NearOut near, PairBounds sure) {
   const int at = blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= a.n) return;
   float lo, hi;
@@ -220,16 +220,13 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
     float lo0, hi0, lo1, hi1;
     band_for(near.cut[0], a.cmax, lo0, hi0);
     band_for(near.cut[1], a.cmax, lo1, hi1);
-    const int si = min(max(int(pfa.w), 0), pb.ns - 1);
+    // sure: the float r^2 below the band's lower edge around (bound - h_q)^2
+    float slo0, shi0, slo1, shi1;
+    band_for(fmax(sure.cut[0] - near.h[0], 0.0), a.cmax, slo0, shi0);
+    band_for(fmax(sure.cut[0] - near.h[1], 0.0), a.cmax, slo1, shi1);
     int w0 = 0, w1 = 0;
     for (int s = 0; s < m; ++s) {
-      const float4 pfb = a.posf[buf[s]];
-      const float r2 = dist2f(pfa, pfb, wrap);
-      const double cut = pb.cut[si * pb.ns + min(max(int(pfb.w), 0), pb.ns - 1)];
-      // sure: the float r^2 below the band's lower edge around (cut - h_q)^2
-      float slo0, shi0, slo1, shi1;
-      band_for(fmax(cut - near.h[0], 0.0), a.cmax, slo0, shi0);
-      band_for(fmax(cut - near.h[1], 0.0), a.cmax, slo1, shi1);
+      const float r2 = dist2f(pfa, a.posf[buf[s]], wrap);
       const unsigned b = unsigned(buf[s]);
       if (!(r2 > hi0)) near.nbr[0][ell_at(w0++, at, a.npad)] = int(b | (r2 < slo0 ? kSure : 0u));
       if (!(r2 > hi1)) near.nbr[1][ell_at(w1++, at, a.npad)] = int(b | (r2 < slo1 ? kSure : 0u));
@@ -552,6 +549,21 @@ PairBounds pair_bounds(const Ctx& c, FilterMode mode) {
   return pb;
 }
 
+// The bound sure bits are tested against: the smallest pair bound of the
+// table (one "species pair"), so that a species change between list builds —
+// set_system keeps the list — cannot make a sure entry wrong.
+PairBounds sure_bound(const Ctx& c, bool near) {
+  PairBounds sb{{}, {}, 1};
+  if (near) {
+    const PairBounds pb = pair_bounds(c, FilterMode::Pair);
+    double m = pb.cut[0];
+    for (int q = 1; q < pb.ns * pb.ns; ++q) m = std::min(m, pb.cut[q]);
+    sb.cut[0] = m;
+    sb.c2[0] = m * m;
+  }
+  return sb;
+}
+
 template <int CAP>
 void launch_skin(Ctx& c, double bc2, int cap) {
   const bool near = c.near_cut[0] > 0.0;
@@ -564,7 +576,7 @@ void launch_skin(Ctx& c, double bc2, int cap) {
               c.flags.get() + 11,
               {c.near_cut[0], c.near_cut[1]},
               {c.near_cut[0] - rf, c.near_cut[1] - rf}},
-      near ? pair_bounds(c, FilterMode::Pair) : PairBounds{{}, {}, 1});
+      sure_bound(c, near));
   ++c.launches;
 }
 

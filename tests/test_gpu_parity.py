@@ -428,5 +428,24 @@ def test_near_list_filter_is_exact(tb, kind, sic_text):
             assert abs(e1 - e2) <= tol * abs(e2), (frac, prec)
             ftol = 1e-12 if prec == "double" else 2e-6 * max(1.0, np.abs(f2).max())
             assert np.abs(f1 - f2).max() <= ftol, (frac, prec)
+    if kind == "sic":
+        # a species change keeps the list (set_system, same n and box): the
+        # sure bits are species-independent, so the lists still agree
+        ctx.set_positions(case.xyz)
+        ctx.build_neighbor_list(params.r_cut_max, case.skin)   # |d|max = 0: near lists
+        skin_off, skin_nb = ctx.export_neighbors("skin")
+        sp = case.species.copy()
+        flip = rng.random(len(sp)) < 0.3
+        sp[flip] = 1 - sp[flip]
+        ctx.set_system(case.xyz, sp, case.box, case.periodic)
+        assert not ctx.needs_rebuild()
+        fresh.set_system(case.xyz, sp, case.box, case.periodic)
+        fresh.set_neighbor_list(skin_off, skin_nb, params.r_cut_max, case.skin)
+        a_off, a_nb = ctx.export_neighbors("short")
+        b_off, b_nb = fresh.export_neighbors("short")
+        assert np.array_equal(a_off, b_off) and np.array_equal(a_nb, b_nb)
+        e1, f1, _ = ctx.compute("double", deterministic=True)
+        e2, f2, _ = fresh.compute("double", deterministic=True)
+        assert abs(e1 - e2) <= 1e-13 * abs(e2) and np.abs(f1 - f2).max() <= 1e-12
     for c in (ctx, fresh):
         c.close()
