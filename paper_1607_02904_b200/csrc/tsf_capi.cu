@@ -273,10 +273,13 @@ void evaluate_launches(Ctx& c, tsf::Precision p, std::uint32_t flags) {
       zb = 8;
     }
   }
+  // the filter launch (none for an empty system) also zeroes flags[0..3]
+  const bool zero_flags = c.n > 0;
   tsf::list_filter(c, (flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair,
-                   zf, zb, 0, -1, true);
+                   zf, zb, 0, -1, zero_flags);
   c.mark(1);
-  tsf::compute(c, p, (zf ? (flags | tsf::kFlagForcesZeroed) : flags) | tsf::kFlagFlagsZeroed);
+  tsf::compute(c, p, (zf ? (flags | tsf::kFlagForcesZeroed) : flags) |
+                         (zero_flags ? tsf::kFlagFlagsZeroed : 0u));
   c.mark(4);
 }
 
