@@ -729,13 +729,18 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   // between rebuilds — take the G=16 / G=32 tier launches.  Measured per-atom
   // costs (B200, f64; profiles/r01): main G=4 0.26 ns, G=8 0.69 ns, G=16
   // 1.7 ns (no register cache of d zeta/d x_k above 8), a queued atom
-  // 2.3-2.6 ns, so G=4 wins below ~15% over-4 atoms and G=8 below ~35%
-  // over-8 (3C-SiC 256k: 45% / 8% -> G=8, 1.8x over G=16; liquid Si
-  // 512k -> G=8, 2.0x).
+  // 2.3-2.6 ns when first measured (about 1 ns with today's tier launches),
+  // so G=4 wins below ~15% over-4 atoms (float; ~50% in f64) and G=8 below
+  // ~35% over-8 (3C-SiC 256k: 45% / 8% -> G=8 float, G=4 f64; liquid Si
+  // 512k -> G=8, 2.0x over G=16).
   const ListState& s = c.short_list;
   const int mx = std::max(1, s.max_count);
   const std::int64_t n = std::max<std::int64_t>(c.n, 1);
-  int g = (mx <= 4 || s.over4 * 100 <= 15 * n) ? 4
+  // FP64's G = 8 (rolled, cache in local memory) costs more next to its G = 4
+  // than float's unrolled G = 8 does: 3C-SiC 256k (45% over 4) runs 3% faster
+  // at G = 4 + tier launches in f64 and 25% slower in float (tools/ab.py)
+  const int over4_pct = std::is_same<R, double>::value ? 50 : 15;
+  int g = (mx <= 4 || s.over4 * 100 <= over4_pct * n) ? 4
           : (mx <= 8 || s.over8 * 100 <= 35 * n) ? 8
           : 16;
   // TSF_GROUP_WIDTH=4|8|16|32 pins the width (tuning and the tier tests)
