@@ -334,13 +334,40 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       }
       if (!active) n_i = 0;
     }
-    if (n_i > G) {
-      if (gl == 0) {
-        if (a.ovf_out) a.ovf_out[atomicAdd(a.ovf_out_count, 1)] = i;
-        else atomicOr(a.flags, kErrShortOverflow);
+    // atoms over the width go to the next tier's queue.  The FP64 G = 4 main
+    // launch (3C-SiC in f64 queues 45% of its atoms) and the tier launches
+    // take one atomic per warp, and a warp's atoms land side by side in slot
+    // order, so the next launch reads neighbouring slots — SiC f64 step -8%
+    // against an atomic per atom (arrival order, every queued atom serialised
+    // on one address).  The other main launches queue few atoms and keep the
+    // per-atom form (tools/ab.py: the vote cost the float G = 4 kernel 1%).
+    if constexpr ((G == 4 && std::is_same<R, double>::value) || OVF) {
+      const bool over = n_i > G;
+      const unsigned lead = __ballot_sync(kFull, over && gl == 0);
+      if (lead) {                      // warp-uniform
+        if (a.ovf_out) {
+          const int first = __ffs(lead) - 1;
+          int base = 0;
+          if (lane == first) base = atomicAdd(a.ovf_out_count, __popc(lead));
+          base = __shfl_sync(kFull, base, first);
+          if (over && gl == 0) a.ovf_out[base + __popc(lead & ((1u << lane) - 1u))] = i;
+        } else if (over && gl == 0) {
+          atomicOr(a.flags, kErrShortOverflow);
+        }
       }
-      n_i = 0;
-      active = false;
+      if (over) {
+        n_i = 0;
+        active = false;
+      }
+    } else {
+      if (n_i > G) {
+        if (gl == 0) {
+          if (a.ovf_out) a.ovf_out[atomicAdd(a.ovf_out_count, 1)] = i;
+          else atomicOr(a.flags, kErrShortOverflow);
+        }
+        n_i = 0;
+        active = false;
+      }
     }
     const bool slot = gl < n_i;
     double dx = 0, dy = 0, dz = 0, r2 = 1.0;
