@@ -305,6 +305,57 @@ bool graphs_enabled() {
   return on;
 }
 
+// Replay slot `slot`'s graph while its key holds; capture it on the second
+// eager run with the same key; else run eagerly.  `launches` must leave the
+// same host state on every run with one key (restored on replay).
+template <typename F>
+void run_graphed(Ctx& c, int slot, bool graphable, const std::uint64_t* key, F&& launches) {
+  Ctx::GraphSlot& s = c.graph[slot];
+  if (graphable && s.exec && std::equal(key, key + 6, s.key)) {
+    TSF_CUDA(cudaGraphLaunch(s.exec, c.stream));
+    c.launches += s.launches;
+    c.phase_blocks = s.phase_blocks;
+    return;
+  }
+  if (!(graphable && std::equal(key, key + 6, s.warm))) {
+    launches();
+    std::copy(key, key + 6, s.warm);
+    return;
+  }
+  if (s.exec) {
+    TSF_CUDA(cudaGraphExecDestroy(s.exec));
+    s.exec = nullptr;
+  }
+  const std::int64_t l0 = c.launches;
+  const int pb0 = c.phase_blocks;
+  cudaGraph_t g = nullptr;
+  bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    try {
+      launches();
+    } catch (...) {
+      ok = false;
+    }
+    ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
+    ok = ok && cudaGraphInstantiate(&s.exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+  }
+  if (ok) {
+    s.launches = c.launches - l0;
+    s.phase_blocks = c.phase_blocks;
+    std::copy(key, key + 6, s.key);
+    TSF_CUDA(cudaGraphLaunch(s.exec, c.stream));
+  } else {   // capture refused: clear the sticky error and stay eager
+    cudaGetLastError();
+    if (s.exec) cudaGraphExecDestroy(s.exec);
+    s.exec = nullptr;
+    c.graphs_off = true;
+    c.launches = l0;
+    c.phase_blocks = pb0;
+    launches();
+  }
+}
+
 // Steady-state evaluations replay a CUDA graph of evaluate_launches: between
 // list rebuilds every launch has the same configuration and arguments (device
 // buffers, group width, grid sizes), so at small N — where ~10 launches and
@@ -325,43 +376,7 @@ void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
                                 std::uint64_t(c.n_owned),
                                 std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
   const bool graphable = graphs_enabled() && !c.graphs_off && !c.profile && steady && c.n > 0;
-  if (graphable && c.graph_exec && std::equal(key, key + 6, c.graph_key)) {
-    TSF_CUDA(cudaGraphLaunch(c.graph_exec, c.stream));
-    c.launches += c.graph_launches;
-  } else if (graphable && std::equal(key, key + 6, c.warm_key)) {
-    if (c.graph_exec) {
-      TSF_CUDA(cudaGraphExecDestroy(c.graph_exec));
-      c.graph_exec = nullptr;
-    }
-    const std::int64_t l0 = c.launches;
-    cudaGraph_t g = nullptr;
-    bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-    if (ok) {
-      try {
-        evaluate_launches(c, p, flags);
-      } catch (...) {
-        ok = false;
-      }
-      ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
-      ok = ok && cudaGraphInstantiate(&c.graph_exec, g, 0) == cudaSuccess;
-      if (g) cudaGraphDestroy(g);
-    }
-    if (ok) {
-      c.graph_launches = c.launches - l0;
-      std::copy(key, key + 6, c.graph_key);
-      TSF_CUDA(cudaGraphLaunch(c.graph_exec, c.stream));
-    } else {   // capture refused: clear the sticky error and stay eager
-      cudaGetLastError();
-      if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
-      c.graph_exec = nullptr;
-      c.graphs_off = true;
-      c.launches = l0;
-      evaluate_launches(c, p, flags);
-    }
-  } else {
-    evaluate_launches(c, p, flags);
-    std::copy(key, key + 6, c.warm_key);
-  }
+  run_graphed(c, 0, graphable, key, [&] { evaluate_launches(c, p, flags); });
   c.forces_current = true;
   if (c.profile) {
     TSF_CUDA(cudaEventSynchronize(c.ev[4]));
@@ -514,7 +529,8 @@ void tsf_destroy(tsf_ctx* ctx) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.pinned) cudaFreeHost(c.pinned);
   c.pinned = nullptr;
-  if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
+  for (auto& g : c.graph)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& e : c.ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = c.own_stream;       // never destroy a caller's stream
@@ -562,10 +578,17 @@ int tsf_compute_phase(tsf_ctx* ctx, int precision, uint32_t flags, int phase) {
       const bool steady = !c.short_max_stale && c.short_apply == mode;
       if (c.split_slots < 0 || !steady || c.profile) return;   // phase 1 does it all
       const int split = int(c.split_slots);
-      set_phase(c, 0, split, true, false);
-      c.phase_blocks = 0;
-      tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, 0, split);
-      tsf::compute(c, p, flags);
+      const std::uint64_t key[6] = {c.list_version, std::uint64_t(p), flags, std::uint64_t(c.n),
+                                    std::uint64_t(split),
+                                    std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
+      // graph-replayed like evaluate(): at 8 ranks a phase's dozen launches
+      // set the pace of a 0.1 ms step (tools/rank_share.py)
+      run_graphed(c, 1, graphs_enabled() && !c.graphs_off && c.n > 0, key, [&] {
+        set_phase(c, 0, split, true, false);
+        c.phase_blocks = 0;
+        tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, 0, split);
+        tsf::compute(c, p, flags);
+      });
       c.phase0_done = true;
       c.forces_current = false;
       return;
@@ -575,9 +598,14 @@ int tsf_compute_phase(tsf_ctx* ctx, int precision, uint32_t flags, int phase) {
       return;
     }
     const int split = int(c.split_slots);
-    set_phase(c, split, int(c.n), false, true);
-    tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, split, int(c.n));
-    tsf::compute(c, p, flags);
+    const std::uint64_t key[6] = {c.list_version, std::uint64_t(p), flags, std::uint64_t(c.n),
+                                  std::uint64_t(split),
+                                  std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
+    run_graphed(c, 2, graphs_enabled() && !c.graphs_off && c.n > 0, key, [&] {
+      set_phase(c, split, int(c.n), false, true);
+      tsf::list_filter(c, tsf::FilterMode(mode), nullptr, 0, split, int(c.n));
+      tsf::compute(c, p, flags);
+    });
     set_phase(c, 0, int(c.n), true, true);
     c.phase0_done = false;
     c.forces_current = true;

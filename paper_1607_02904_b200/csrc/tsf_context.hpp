@@ -173,10 +173,15 @@ struct Ctx {
   // CUDA graph of the steady-state evaluation (filter + force launches),
   // replayed while its key holds; see evaluate() in tsf_capi.cu
   std::uint64_t list_version = 0;      // bumped by every list / centre-set change
-  cudaGraphExec_t graph_exec = nullptr;
-  std::uint64_t graph_key[6] = {};     // key of graph_exec
-  std::uint64_t warm_key[6] = {};      // key of the last eager evaluation
-  std::int64_t graph_launches = 0;     // kernels per replay
+  // (slot 0: a whole evaluation; 1 and 2: the two phases of a split one)
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    std::uint64_t key[6] = {};         // key of exec
+    std::uint64_t warm[6] = {};        // key of the last eager run
+    std::int64_t launches = 0;         // kernels per replay
+    int phase_blocks = 0;              // host state the launches leave behind
+  };
+  GraphSlot graph[3];
   bool graphs_off = false;             // capture failed once: stay eager
 
   // MD state

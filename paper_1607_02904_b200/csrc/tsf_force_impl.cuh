@@ -594,23 +594,36 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   }
 }
 
-// Sum of the block partials in a fixed order.
-__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partials, int nblocks,
-                                               double* __restrict__ out) {
-  __shared__ double s[256][7];
+// Sum of the block partials in a fixed order: 1024 threads stride over the
+// blocks (one pass at the usual few hundred to two thousand partials), warp
+// shuffles, then warp 0 over the 32 warp sums — one barrier instead of the
+// ten of a shared-memory tree (the reduction is on every step's critical path).
+__global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int nblocks,
+                                                double* __restrict__ out) {
+  __shared__ double s[32][8];
   griddep_wait();
   const int t = threadIdx.x;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = t; b < nblocks; b += 256)
+  for (int b = t; b < nblocks; b += 1024)
+#pragma unroll
     for (int q = 0; q < 7; ++q) acc[q] += partials[std::size_t(b) * kRedWidth + q];
-  for (int q = 0; q < 7; ++q) s[t][q] = acc[q];
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_down_sync(kFull, acc[q], o);
+  if ((t & 31) == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) s[t >> 5][q] = acc[q];
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (t < w)
-      for (int q = 0; q < 7; ++q) s[t][q] += s[t + w][q];
-    __syncthreads();
+  if (t < 32) {
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      double v = s[t][q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
+      if (t == 0) out[q] = v;
+    }
   }
-  if (t < 7) out[t] = s[0][t];
 }
 
 // Deterministic mode: energy + virial of the atoms the tier launches took,
@@ -823,7 +836,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
       ++c.launches;
     }
   }
-  launch_pdl(k_reduce, 1, 256, c.stream, static_cast<const double*>(c.partials.get()), nb,
+  launch_pdl(k_reduce, 1, 1024, c.stream, static_cast<const double*>(c.partials.get()), nb,
              c.result.get());
   ++c.launches;
 }

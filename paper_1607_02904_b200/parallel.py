@@ -34,6 +34,7 @@ from . import _lib as L
 from .api import Context, ConfigError, _check
 
 TAG_FWD_LEFT, TAG_FWD_RIGHT, TAG_REV_RIGHT, TAG_REV_LEFT = 11, 12, 13, 14
+TAG_FWD_LEFT2, TAG_FWD_RIGHT2 = 15, 16      # ghost-centre mode: layer-2 ghosts
 
 
 @dataclass
@@ -244,6 +245,7 @@ class Decomposition:
         self.n_owned = len(self.gid)
         dev = self._device()
         self.n_gl1 = self.n_gr1 = 0              # layer-1 ghosts (ghost_centers)
+        self.nl1 = self.nr1 = 0                  # layer-1 atoms among those sent
         if self.world == 1:
             self.send_left = self.send_right = np.zeros(0, np.int64)
             self.n_gl = self.n_gr = 0
@@ -255,10 +257,10 @@ class Decomposition:
                 idx = np.nonzero(near_sel(xyz[:, 0]))[0]
                 l1 = near_l1(xyz[idx, 0])
                 return idx[np.argsort(~l1, kind="stable")], int(l1.sum())   # layer 1 first
-            self.send_left, nl1 = select(self.slab_sel.near_left, self.slab.near_left)
-            self.send_right, nr1 = select(self.slab_sel.near_right, self.slab.near_right)
+            self.send_left, self.nl1 = select(self.slab_sel.near_left, self.slab.near_left)
+            self.send_right, self.nr1 = select(self.slab_sel.near_right, self.slab.near_right)
             (self.n_gl, self.n_gl1), (self.n_gr, self.n_gr1) = self._swap_counts(
-                (len(self.send_left), nl1), (len(self.send_right), nr1))
+                (len(self.send_left), self.nl1), (len(self.send_right), self.nr1))
             if not self.ghost_centers:
                 self.n_gl1 = self.n_gr1 = 0
             # ghost payload: global id, species, xyz (as float64 rows)
@@ -289,8 +291,36 @@ class Decomposition:
         def buf(m):
             return torch.empty((m, 3), dtype=torch.float64, device=dev)
         nl, nr = len(self.send_left), len(self.send_right)
-        self._pos_send_l, self._pos_send_r = buf(nl), buf(nr)
-        self._pos_from_l, self._pos_from_r = buf(self.n_gl), buf(self.n_gr)
+        # forward exchange: ONE gather launch fills [to left | to right], the
+        # receives land straight in local ghost order, ONE scatter launch
+        # writes them (small launches were a third of a rank's step at 8 GPUs,
+        # tools/rank_share.py)
+        self.t_send = torch.cat([self.t_send_left, self.t_send_right])
+        self._pos_send = buf(nl + nr)
+        self._ghost_in = buf(self.n_gl + self.n_gr)
+        send_l, send_r = self._pos_send[:nl], self._pos_send[nl:]
+        if self.ghost_centers:
+            # a sender's lists hold layer 1 first; [l1 | l2] goes out as two
+            # messages per side so that the receiver's four blocks are in place
+            ll1, lr1 = self.nl1, self.nr1
+            g = self._ghost_in
+            a, b = self.n_gl1, self.n_gl1 + self.n_gr1
+            c = b + (self.n_gl - self.n_gl1)
+            from_l1, from_r1, from_l2, from_r2 = g[:a], g[a:b], g[b:c], g[c:]
+            self._fwd_sends = [(send_l[:ll1], self.left, TAG_FWD_LEFT),
+                               (send_l[ll1:], self.left, TAG_FWD_LEFT2),
+                               (send_r[:lr1], self.right, TAG_FWD_RIGHT),
+                               (send_r[lr1:], self.right, TAG_FWD_RIGHT2)]
+            self._fwd_recvs = [(from_r1, self.right, TAG_FWD_LEFT),
+                               (from_r2, self.right, TAG_FWD_LEFT2),
+                               (from_l1, self.left, TAG_FWD_RIGHT),
+                               (from_l2, self.left, TAG_FWD_RIGHT2)]
+        else:
+            from_l, from_r = self._ghost_in[:self.n_gl], self._ghost_in[self.n_gl:]
+            self._fwd_sends = [(send_l, self.left, TAG_FWD_LEFT),
+                               (send_r, self.right, TAG_FWD_RIGHT)]
+            self._fwd_recvs = [(from_r, self.right, TAG_FWD_LEFT),
+                               (from_l, self.left, TAG_FWD_RIGHT)]
         self._f_ghost_l, self._f_ghost_r = buf(self.n_gl), buf(self.n_gr)
         self._f_to_l, self._f_to_r = buf(nl), buf(nr)
 
@@ -299,15 +329,9 @@ class Decomposition:
         """Refresh ghost positions from their owners."""
         if self.world == 1:
             return
-        send_l = self.engine.gather_positions(self.t_send_left, out=self._pos_send_l)
-        send_r = self.engine.gather_positions(self.t_send_right, out=self._pos_send_r)
-        from_l, from_r = self._pos_from_l, self._pos_from_r
-        self._exchange([(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
-                       [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
-        lo = self.n_owned
-        for block in self._layout(from_l, from_r):
-            self.engine.scatter_positions(lo, block)
-            lo += len(block)
+        self.engine.gather_positions(self.t_send, out=self._pos_send)
+        self._exchange(self._fwd_sends, self._fwd_recvs)
+        self.engine.scatter_positions(self.n_owned, self._ghost_in)
 
     def _layout(self, from_l, from_r):
         """Received ghost rows in local order: classic [left | right];
@@ -335,18 +359,11 @@ class Decomposition:
         if self.overlap and self.world > 1:
             # ghosts in flight while the interior centres compute (phase 0;
             # a no-op when the engine cannot split yet — phase 1 then does it all)
-            send_l = self.engine.gather_positions(self.t_send_left, out=self._pos_send_l)
-            send_r = self.engine.gather_positions(self.t_send_right, out=self._pos_send_r)
-            from_l, from_r = self._pos_from_l, self._pos_from_r
-            reqs = self._exchange_start(
-                [(send_l, self.left, TAG_FWD_LEFT), (send_r, self.right, TAG_FWD_RIGHT)],
-                [(from_r, self.right, TAG_FWD_LEFT), (from_l, self.left, TAG_FWD_RIGHT)])
+            self.engine.gather_positions(self.t_send, out=self._pos_send)
+            reqs = self._exchange_start(self._fwd_sends, self._fwd_recvs)
             self.engine.compute_phase(0, precision, deterministic)
             self._exchange_finish(reqs)
-            lo = self.n_owned
-            for block in self._layout(from_l, from_r):
-                self.engine.scatter_positions(lo, block)
-                lo += len(block)
+            self.engine.scatter_positions(self.n_owned, self._ghost_in)
             self.engine.compute_phase(1, precision, deterministic)
         else:
             self.forward()
