@@ -321,8 +321,12 @@ class Decomposition:
                                (send_r, self.right, TAG_FWD_RIGHT)]
             self._fwd_recvs = [(from_r, self.right, TAG_FWD_LEFT),
                                (from_l, self.left, TAG_FWD_RIGHT)]
-        self._f_ghost_l, self._f_ghost_r = buf(self.n_gl), buf(self.n_gr)
-        self._f_to_l, self._f_to_r = buf(nl), buf(nr)
+        # reverse exchange (classic mode): one gather of the ghost forces
+        # [left | right] and, unless an atom is sent both ways (slabs of
+        # exactly 2 halo), one add over [from left | from right]
+        self._f_ghost = buf(self.n_gl + self.n_gr)
+        self._f_to = buf(nl + nr)
+        self._rev_fused = len(np.intersect1d(self.send_left, self.send_right)) == 0
 
     # ---- one force evaluation ------------------------------------------
     def forward(self):
@@ -346,14 +350,18 @@ class Decomposition:
         mode; with ghost_centers the owned forces are already complete)."""
         if self.world == 1 or self.ghost_centers:
             return
-        f_gl = self.engine.ghost_forces(self.n_owned, self.n_gl, out=self._f_ghost_l)
-        f_gr = self.engine.ghost_forces(self.n_owned + self.n_gl, self.n_gr, out=self._f_ghost_r)
-        to_l, to_r = self._f_to_l, self._f_to_r
+        f_g = self.engine.ghost_forces(self.n_owned, self.n_gl + self.n_gr, out=self._f_ghost)
+        f_gl, f_gr = f_g[:self.n_gl], f_g[self.n_gl:]
+        nl = len(self.send_left)
+        to_l, to_r = self._f_to[:nl], self._f_to[nl:]
         # my right ghosts are the right neighbour's send_left; my left ghosts its send_right
         self._exchange([(f_gr, self.right, TAG_REV_RIGHT), (f_gl, self.left, TAG_REV_LEFT)],
                        [(to_l, self.left, TAG_REV_RIGHT), (to_r, self.right, TAG_REV_LEFT)])
-        self.engine.add_forces(self.t_send_left, to_l)
-        self.engine.add_forces(self.t_send_right, to_r)
+        if self._rev_fused:
+            self.engine.add_forces(self.t_send, self._f_to)
+        else:
+            self.engine.add_forces(self.t_send_left, to_l)
+            self.engine.add_forces(self.t_send_right, to_r)
 
     def evaluate(self, precision: str = "double", deterministic: bool = False):
         if self.overlap and self.world > 1:

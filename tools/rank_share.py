@@ -58,6 +58,8 @@ def make_rank(text, xyz, species, box, per, world, rank, mail, out, skin):
         dec.rank, dec.world = rank, world
         dec.box, dec.periodic = np.asarray(box, np.float64), np.asarray(per, np.uint8)
         gc = world > 1 and box[0] / world >= 4 * halo          # bench.py's rule
+        if os.environ.get("RS_GC") == "0":                     # classic mode: reverse exchange
+            gc = False
         # RS_OVERLAP=0: the one-phase step (graph-replayed evaluation after a
         # blocking exchange) instead of bench.py's overlapped split
         dec.ghost_centers = gc
@@ -126,6 +128,7 @@ def main():
     skin = 1.0
     res = {"config": cfg, "n_atoms": len(xyz), "steps": steps, "precision": {},
            "overlap": os.environ.get("RS_OVERLAP", "1") != "0",
+           "ghost_centres_allowed": os.environ.get("RS_GC") != "0",
            "note": "projection on ONE B200: each rank's step timed alone, NCCL transfer "
                    "excluded (tools/rank_share.py)"}
     for precision in os.environ.get("RS_PRECISIONS", "double,mixed").split(","):
