@@ -594,35 +594,29 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   }
 }
 
-// Sum of the block partials in a fixed order: 1024 threads stride over the
-// blocks (one pass at the usual few hundred to two thousand partials), warp
-// shuffles, then warp 0 over the 32 warp sums — one barrier instead of the
-// ten of a shared-memory tree (the reduction is on every step's critical path).
+// Sum of the block partials in a fixed order.  The partials are read as one
+// flat array: thread t always holds quantity q = t % 8 (1024 % kRedWidth == 0),
+// so every warp load is 256 contiguous bytes; lanes of equal q meet in two
+// shuffles, the 32 warps' sums in shared memory — the reduction sits on every
+// step's critical path, and at 32k atoms it was a quarter of the step.
+static_assert(kRedWidth == 8, "k_reduce maps one quantity per thread mod 8");
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int nblocks,
                                                 double* __restrict__ out) {
-  __shared__ double s[32][8];
+  __shared__ double s[32][kRedWidth];
   griddep_wait();
   const int t = threadIdx.x;
-  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = t; b < nblocks; b += 1024)
-#pragma unroll
-    for (int q = 0; q < 7; ++q) acc[q] += partials[std::size_t(b) * kRedWidth + q];
-#pragma unroll
-  for (int q = 0; q < 7; ++q)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_down_sync(kFull, acc[q], o);
-  if ((t & 31) == 0)
-#pragma unroll
-    for (int q = 0; q < 7; ++q) s[t >> 5][q] = acc[q];
+  const int total = nblocks * kRedWidth;
+  double acc = 0;
+  for (int e = t; e < total; e += 1024) acc += partials[e];
+  acc += __shfl_xor_sync(kFull, acc, 8);
+  acc += __shfl_xor_sync(kFull, acc, 16);
+  if ((t & 31) < kRedWidth) s[t >> 5][t & 31] = acc;
   __syncthreads();
-  if (t < 32) {
-#pragma unroll
-    for (int q = 0; q < 7; ++q) {
-      double v = s[t][q];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
-      if (t == 0) out[q] = v;
-    }
+  if (t < 7) {
+    double v = 0;
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) v += s[w][t];
+    out[t] = v;
   }
 }
 
