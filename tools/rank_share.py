@@ -117,7 +117,17 @@ def time_rank(eng, dec, stream, precision, steps):
                 eng.compute_phase(1, precision)
             torch.cuda.synchronize()
             phase0_ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-    return step_ms, phase0_ms, host_ms
+        # stage split of the (one-phase) evaluation: profiling runs eagerly,
+        # event-timed per stage (filter / setup / main force launch / tiers +
+        # reduction) — the diagnostic behind the fixed per-step cost
+        eng.ctx.profile(True)
+        for _ in range(steps):
+            dec.evaluate(precision)
+        prof = eng.ctx.profile_read(reset=True)
+        eng.ctx.profile(False)
+        calls = max(prof["calls"], 1)
+        stages = {k: prof[k] / calls for k in ("filter_ms", "setup_ms", "force_ms", "tail_ms")}
+    return step_ms, phase0_ms, host_ms, stages
 
 
 def main():
@@ -148,11 +158,12 @@ def main():
             only = os.environ.get("RS_RANKS")       # time a subset (ncu runs)
             for r in (range(world) if not only else range(min(int(only), world))):
                 eng, dec, stream = out[r]
-                step_ms, p0_ms, host_ms = time_rank(eng, dec, stream, precision, steps)
+                step_ms, p0_ms, host_ms, stages = time_rank(eng, dec, stream, precision, steps)
                 sent = 24 * (len(dec.send_left) + len(dec.send_right))
                 per_rank.append({"rank": r, "owned": dec.n_owned, "ghosts": len(dec.ghost_gid),
                                  "centres": dec.n_centers, "interior": dec.n_interior,
                                  "step_ms": step_ms, "phase0_ms": p0_ms, "host_enqueue_ms": host_ms,
+                                 "stages_one_phase": stages,
                                  "send_bytes_per_step": sent})
             gcent = bool(out[0][1].ghost_centers)
             for r in range(world):
