@@ -168,6 +168,8 @@ struct Ctx {
   bool phase_first = true, phase_last = true;
   int phase_blocks = 0;                // partial blocks written by earlier phases
   std::int64_t split_slots = -1;       // interior slots [0, split) of the current list
+  std::int64_t center_slots = -1;      // list built with centres first: slots [0, this) hold
+                                       // every centre, non-centre ghosts follow (else -1)
   bool phase0_done = false;            // phase 0 ran; phase 1 completes the evaluation
 
   // CUDA graph of the steady-state evaluation (filter + force launches),

@@ -866,6 +866,11 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.center_limit = int(c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n);
   a.energy_limit = c.n_energy >= 0 ? int(std::min<std::int64_t>(c.n_energy, a.center_limit))
                                    : a.center_limit;
+  // the list build put every centre below center_slots (non-centre ghosts
+  // behind them): atomic mode stops the launches there.  Deterministic mode
+  // keeps the ghost slots — the force launch zeroes their self terms there.
+  if (!det && c.center_slots >= 0 && c.center_slots == a.center_limit)
+    a.n_owned = std::min(a.n_owned, int(c.center_slots));
   a.npad = npad;
   a.box = c.box;
   a.nbr = c.short_list.nbr.get();

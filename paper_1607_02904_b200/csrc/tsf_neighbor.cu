@@ -59,8 +59,10 @@ __device__ __forceinline__ void warp_atomic_max(int* p, int v) {
 // key is class-major: user atoms below n_int (interior owned) sort first, so
 // their slots are [0, n_int); the "cell" index is then class * ncells + cell,
 // keeping every (class, cell) run contiguous for the skin build.
+// Non-centre ghosts (user index >= n_ctr, decompositions) form the last class,
+// so every centre holds a slot below n_ctr and the force launches stop there.
 __global__ void k_cell_key(const double4* __restrict__ pos, const int* __restrict__ perm, int n,
-                           CellGrid g, int n_int, unsigned long long* __restrict__ keys,
+                           CellGrid g, int n_int, int n_ctr, unsigned long long* __restrict__ keys,
                            int* __restrict__ vals, int* __restrict__ count,
                            int* __restrict__ max_occ) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -71,8 +73,9 @@ __global__ void k_cell_key(const double4* __restrict__ pos, const int* __restric
   const int cz = clamp_cell(p.z, g.org[2], g.ext[2], g.nc[2]);
   const unsigned user = unsigned(perm ? perm[s] : s);
   const int ncells = g.nc[0] * g.nc[1] * g.nc[2];
-  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx +
-                (n_int >= 0 && int(user) >= n_int ? ncells : 0);
+  int cls = n_int >= 0 && int(user) >= n_int ? 1 : 0;
+  if (n_ctr >= 0 && int(user) >= n_ctr) cls = n_int >= 0 ? 2 : 1;
+  const int c = (cz * g.nc[1] + cy) * g.nc[0] + cx + cls * ncells;
   keys[s] = (static_cast<unsigned long long>(c) << 32) | user;
   vals[s] = s;
   warp_atomic_max(max_occ, atomicAdd(count + c, 1) + 1);
@@ -504,6 +507,18 @@ void swap_buf(DevBuf<T>& a, DevBuf<T>& b) {
   std::swap(a.cap, b.cap);
 }
 
+// Slot classes of a list build: [interior owned] [other centres] [non-centre
+// ghosts] — the first only with an interior split, the last only when the
+// context has ghosts (tsf_set_owned / tsf_set_centers below n).
+int ghost_class_limit(const Ctx& c) {
+  const std::int64_t lim = c.n_owned >= 0 ? std::min<std::int64_t>(c.n_owned, c.n) : c.n;
+  return lim < c.n ? int(lim) : -1;
+}
+
+int slot_classes(const Ctx& c) {
+  return (c.n_interior >= 0 ? 2 : 1) + (ghost_class_limit(c) >= 0 ? 1 : 0);
+}
+
 ListArgs list_args(Ctx& c) {
   ListArgs a;
   a.pos = c.pos.get();
@@ -516,7 +531,7 @@ ListArgs list_args(Ctx& c) {
   a.g = c.grid;
   a.cell_of = c.cell_of.get();
   a.start = c.cell_start.get();
-  a.ncls = c.n_interior >= 0 ? 2 : 1;
+  a.ncls = slot_classes(c);
   return a;
 }
 
@@ -653,8 +668,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
     g.ext[ax] = hi[ax] - lo[ax];
     g.nc[ax] = std::max(1, int(std::floor(g.ext[ax] / bc)));
   }
-  const std::int64_t ncells =
-      std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2] * (c.n_interior >= 0 ? 2 : 1);
+  const std::int64_t ncells = std::int64_t(g.nc[0]) * g.nc[1] * g.nc[2] * slot_classes(c);
   if (ncells > (1ll << 30)) throw ConfigError("cell grid too large");
 
   // ---- re-sort the atoms by (cell, user index) ----
@@ -684,7 +698,8 @@ void list_build(Ctx& c, double cutoff, double skin) {
   if (n > 0) {
     k_cell_key<<<blocks_for(n), kBlock, 0, c.stream>>>(
         c.pos.get(), c.sorted ? c.perm.get() : nullptr, n, g,
-        c.n_interior >= 0 ? int(std::min<std::int64_t>(c.n_interior, n)) : -1, c.sort_keys.get(),
+        c.n_interior >= 0 ? int(std::min<std::int64_t>(c.n_interior, n)) : -1,
+        ghost_class_limit(c), c.sort_keys.get(),
         c.sort_vals.get(), c.cell_count.get(), c.flags.get() + 6);
     ++c.launches;
     TSF_CUDA(cub::DeviceRadixSort::SortPairs(c.scan_tmp.get(), t_sort, c.sort_keys.get(),
@@ -763,6 +778,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
   ++c.list_version;
   // interior atoms hold slots [0, n_interior) after a split build
   c.split_slots = c.n_interior >= 0 ? std::min<std::int64_t>(c.n_interior, n) : -1;
+  c.center_slots = ghost_class_limit(c);
 }
 
 void snapshot_reference_positions(Ctx& c) {
