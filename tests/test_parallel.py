@@ -122,7 +122,8 @@ def _case(cells):
     return systems.perturbed(tb, cells, 0.15, 17, skin=0.5)
 
 
-def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False, overlap=False):
+def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False, overlap=False,
+            rev_split=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -134,6 +135,9 @@ def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False, over
         dec = Decomposition(OracleEngine(Oracle(), c.params_text), c.box, c.periodic, halo,
                             ghost_centers=ghost_centers, overlap=overlap)
         dec.setup(gid, c.xyz[gid], c.species[gid], 3.2, c.skin)
+        if rev_split:
+            # the reverse add's fallback (an atom sent both ways): one add per side
+            dec._rev_fused = False
         if shift is not None:
             # move owned atoms a little: the forward exchange must refresh ghosts
             moved = np.mod(c.xyz + shift, c.box)
@@ -159,7 +163,7 @@ def _free_port():
     (2, 6, True, True, False), (3, 9, False, True, False),
     (2, 5, True, False, True), (2, 6, True, True, True)])
 def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifted, ghost_centers,
-                                          overlap):
+                                          overlap, rev_split=False):
     """Classic mode (reverse force exchange) and ghost-centre mode (layer-1
     ghosts act as centres, no reverse exchange) both give the single-process
     energy, forces and virial."""
@@ -167,8 +171,8 @@ def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifte
     c = _case(cells)
     shift = np.array([0.03, -0.02, 0.01]) if shifted else None
     out = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out, ghost_centers, overlap),
-             nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cells, shift, out, ghost_centers, overlap,
+                            rev_split), nprocs=world, join=True)
     res = np.load(out)
     op = parse_param_text(c.params_text)
     off, nb = oracle.build_neighbor_list(c.xyz, c.box, c.periodic, op.r_cut_max, c.skin)
@@ -178,6 +182,12 @@ def test_decomposed_equals_single_process(oracle, tmp_path, world, cells, shifte
     assert abs(res["e"] - ref["energy"]) <= 1e-12 * abs(ref["energy"])
     assert np.abs(res["f"] - ref["forces"]).max() <= 1e-10
     assert np.abs(res["w"] - ref["virial"]).max() <= 1e-10 * np.abs(ref["virial"]).max()
+
+
+def test_reverse_exchange_split_add(oracle, tmp_path):
+    """Classic mode with the reverse add issued per side (the fallback when an
+    atom is sent both ways) equals the fused single add."""
+    test_decomposed_equals_single_process(oracle, tmp_path, 3, 5, True, False, False, True)
 
 
 def test_slab_geometry_guards():
