@@ -43,15 +43,13 @@ CONFIGS = {
     "sic256k": ((32, 32, 32), 4.32, 0.10, "sic",
                 "BASELINE cfg 3: 3C-SiC zincblende 32^3 = 262,144 atoms"),
     "liquid512k": ((40, 40, 40), 5.431, 0.0, "si",
-                   "BASELINE cfg 5: liquid Si 40^3 cells = 512,000 atoms, melted at 6000 K "
-                   "(2 ps) and held at 3000 K (4 ps), dt 0.5 fs, velocity rescaling every 50 "
-                   "steps (SURVEY.md 8d)"),
+                   "BASELINE cfg 5: liquid Si 40^3 cells = 512,000 atoms at 3000 K, the "
+                   "committed snapshot tests/golden/liquid512k.tsfsnap (melted at 6000 K for "
+                   "2 ps, held at 3000 K for 4 ps, dt 0.5 fs, velocity rescaling every 50 "
+                   "steps; SURVEY.md 8d, tools/make_liquid_snapshot.py)"),
 }
-# --impl reference / cpu_baseline: the same workload (lattice, jitter, skin,
-# parameters) at a bounded size, so a --steps K run of the reference's CPU
-# path ends within minutes (the path is O(N): atom-steps/s is size-independent)
-REF_SAMPLE_CELLS = {"si2m": (40, 40, 10), "si32k": (20, 20, 10), "sic256k": (20, 20, 20),
-                    "liquid512k": (25, 25, 25)}
+# --impl reference: the full workload; at ~1 s per step (2M atoms, 16
+# threads) the timed steps are capped so a large --steps ends within minutes
 REF_TIME_CAP_S = 240.0
 DTYPES = {"double": "f64", "mixed": "f32 compute / f64 accumulate", "single": "f32"}
 REF_OPTS = {"double": ("v1", "opt-d", 4), "mixed": ("v2", "opt-m", 8),
@@ -63,27 +61,57 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_system(cfg: str, cells=None):
-    """Synthetic input of the workload: diamond (or zincblende) lattice with a
-    seeded uniform thermal-like jitter (positions wrapped into the box);
-    `cells` overrides the size (the reference arm's bounded sample)."""
-    import paper_1607_02904_b200 as tb
-    full_cells, a0, jitter, pkind, _ = CONFIGS[cfg]
-    s = tb.make_diamond_lattice(*(cells or full_cells), a0)
+LIQUID_SNAPSHOT = os.path.join(ROOT, "tests", "golden", "liquid512k.tsfsnap")
+
+
+def _jitter(xyz, box, cfg):
+    """The seeded uniform thermal-like jitter of the lattice configs, wrapped
+    into the box (tests/systems.py baseline_cfg3/4 build the same arrays)."""
+    jitter = CONFIGS[cfg][2]
     rng = np.random.default_rng(12345)
-    xyz = np.mod(s.positions + rng.uniform(-jitter, jitter, s.positions.shape), s.box.lengths)
-    if cfg.startswith("liquid"):
-        # input preparation (untimed): the GPU melt protocol of SURVEY.md 8d cfg 5
-        xyz = tb.melt(s, tb.builtin_silicon()).positions
-    if pkind == "sic":
+    return np.ascontiguousarray(np.mod(xyz + rng.uniform(-jitter, jitter, xyz.shape), box))
+
+
+def _species_of(cfg, n, species):
+    if CONFIGS[cfg][3] == "sic":
         text = open(os.path.join(ROOT, "tests", "golden", "SiC.tersoff")).read()
-        species = np.where(np.arange(s.natoms) % 8 < 4, 0, 1).astype(np.int32)
-        masses = [28.0855, 12.011]
-    else:
-        text = tb.builtin_silicon().serialize()
-        species = s.species
-        masses = [28.0855]
-    return text, np.ascontiguousarray(xyz), species, s.box.lengths, s.box.periodic, masses
+        return text, np.where(np.arange(n) % 8 < 4, 0, 1).astype(np.int32), [28.0855, 12.011]
+    return None, np.ascontiguousarray(species, np.int32), [28.0855]
+
+
+def make_system(cfg: str):
+    """Synthetic input of the workload through the product's generators:
+    diamond (or zincblende) lattice + seeded jitter, or, for the liquid, the
+    committed TSFSNAP1 snapshot (tools/make_liquid_snapshot.py)."""
+    import paper_1607_02904_b200 as tb
+    if cfg.startswith("liquid"):
+        s = tb.load_snapshot(LIQUID_SNAPSHOT)
+        return (tb.builtin_silicon().serialize(), s.positions, s.species, s.box.lengths,
+                s.box.periodic, list(s.species_masses))
+    cells, a0 = CONFIGS[cfg][0], CONFIGS[cfg][1]
+    s = tb.make_diamond_lattice(*cells, a0)
+    xyz = _jitter(s.positions, s.box.lengths, cfg)
+    text, species, masses = _species_of(cfg, s.natoms, s.species)
+    return (text or tb.builtin_silicon().serialize(), xyz, species, s.box.lengths,
+            s.box.periodic, masses)
+
+
+def make_system_reference(cfg: str, R):
+    """The same arrays without loading the product (the reference arm): the
+    reference's own make_diamond_lattice (engine.cpp:28-58, via oracle/_ref)
+    + the same numpy jitter, or the snapshot through the numpy reader."""
+    from oracle.oracle import SI_TEXT
+    if cfg.startswith("liquid"):
+        from oracle import snapshot as osnap
+        d = osnap.read(LIQUID_SNAPSHOT)
+        return SI_TEXT, d["positions"], d["species"], d["box"], d["periodic"], list(d["masses"])
+    cells, a0 = CONFIGS[cfg][0], CONFIGS[cfg][1]
+    h = R.diamond_lattice(*cells, a0)
+    xyz, _, species, box, per = R.system_arrays(h)
+    R.free_system(h)
+    xyz = _jitter(xyz, box, cfg)
+    text, species, masses = _species_of(cfg, len(xyz), species)
+    return text or SI_TEXT, xyz, species, box, per, masses
 
 
 def algorithmic_work(xyz, species, box, offsets, nbrs, rows, ns):
@@ -221,7 +249,7 @@ def run_reference(args):
                           "oracle/_ref/libtmdref.so not built (run __graft_entry__.build())"}))
         return
     R = Reference()
-    text, xyz, species, box, per, masses = make_system(args.config, REF_SAMPLE_CELLS[args.config])
+    text, xyz, species, box, per, masses = make_system_reference(args.config, R)
     n = len(xyz)
     ph = R.params(text)
     sh = R.system(xyz, species, masses, box, per)
@@ -239,16 +267,16 @@ def run_reference(args):
     t = time.perf_counter() - t0
     value = n * timed / t
     sample = (f"evaluate_forces({scheme}, width {width}, {prec}, workers={cores}) per step on "
-              f"a {n}-atom sample of the same workload ({'x'.join(map(str, REF_SAMPLE_CELLS[args.config]))}"
-              f" cells, same jitter and skin); {timed} of {args.steps} steps timed"
+              f"the full {n}-atom workload (same arrays as the GPU arm, built by the "
+              f"reference's own generator); {timed} of {args.steps} steps timed"
               f"{' (time cap)' if timed < args.steps else ''}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / timed,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": DTYPES[args.precision], "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][4], "precision": args.precision,
-                   "sample_atoms": n},
+        "config": {"workload": CONFIGS[args.config][4], "n_atoms": n,
+                   "precision": args.precision},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -82,6 +82,25 @@ int tsf_perturbed_lattice(const tsf_params* p, int cells, double jitter, uint64_
 int tsf_init_velocities(int64_t n, const int32_t* species, const double* masses,
                         double temperature, uint64_t seed, double* vel);
 
+/* ---- on-disk snapshots (fixtures for thermal and liquid states) ---------
+ * SURVEY.md 8f row 4; the reference regenerates fixtures from seeds
+ * (engine.cpp:28-116, verify.cpp:83-104) and has no file format.  Layout in
+ * csrc/tsf_snapshot.cpp: header, masses, coordinates (float64, or float32
+ * with TSF_SNAP_F32_COORDS — the stored state is then the float32-rounded
+ * one), uint8 species, optional velocities, SHA-256 trailer of every byte
+ * before it.  Readers verify the checksum (TSF_ERR_CONFIG on mismatch). */
+#define TSF_SNAP_F32_COORDS 0x1u
+#define TSF_SNAP_VELOCITIES 0x2u
+int tsf_snapshot_write(const char* path, int64_t n, const double* xyz, const int32_t* species,
+                       int nspecies, const double* masses, const double box[3],
+                       const uint8_t periodic[3], const double* vel /* NULL unless flagged */,
+                       uint32_t flags, uint8_t sha256_out[32] /* may be NULL */);
+int tsf_snapshot_info(const char* path, int64_t* n, int* nspecies, uint32_t* flags,
+                      uint8_t sha256_out[32] /* may be NULL */);
+/* any output may be NULL; vel is zero-filled when the file has none */
+int tsf_snapshot_read(const char* path, double* xyz, int32_t* species, double* masses,
+                      double box[3], uint8_t periodic[3], double* vel);
+
 /* ---- device context -------------------------------------------------- */
 /* p may be NULL: a list-only context (neighbor lists and rebuild checks, no
  * force evaluation), for build_neighbor_list, which takes no parameters. */

@@ -27,6 +27,9 @@ from .api import (  # noqa: F401
     parse_params,
     perturbed_lattice,
     run_nve,
+    load_snapshot,
+    save_snapshot,
+    snapshot_info,
     temperature,
     total_momentum,
 )

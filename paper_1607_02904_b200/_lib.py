@@ -61,6 +61,11 @@ PROTOTYPES = [
                                           _vp]),
     ("tsf_perturbed_lattice", C.c_int, [_vp, C.c_int, _d, C.c_uint64, _vp, _vp, _vp, _vp]),
     ("tsf_init_velocities", C.c_int, [C.c_int64, _vp, _vp, _d, C.c_uint64, _vp]),
+    ("tsf_snapshot_write", C.c_int, [C.c_char_p, C.c_int64, _vp, _vp, C.c_int, _vp, _vp, _vp,
+                                     _vp, C.c_uint32, _vp]),
+    ("tsf_snapshot_info", C.c_int, [C.c_char_p, _i64p, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_uint32), _vp]),
+    ("tsf_snapshot_read", C.c_int, [C.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("tsf_create", C.c_int, [_vp, C.c_int, _pp]),
     ("tsf_destroy", None, [_vp]),
     ("tsf_stream", _vp, [_vp]),

@@ -252,6 +252,53 @@ def total_momentum(system: AtomSystem):
 
 
 # --------------------------------------------------------------------------
+# on-disk snapshots (tsf_snapshot_*; format in csrc/tsf_snapshot.cpp)
+# --------------------------------------------------------------------------
+SNAP_F32_COORDS = 0x1
+SNAP_VELOCITIES = 0x2
+
+
+def save_snapshot(path: str, system: AtomSystem, float32_coords: bool = False,
+                  velocities: bool = False) -> str:
+    """Write `system` (positions, species, masses, box[, velocities]) with a
+    SHA-256 trailer; returns the hex digest.  With float32_coords the stored
+    state is the float32-rounded one — reload the file to get it."""
+    ns = len(system.species_masses)
+    m = np.ascontiguousarray(system.species_masses, dtype=np.float64)
+    flags = (SNAP_F32_COORDS if float32_coords else 0) | (SNAP_VELOCITIES if velocities else 0)
+    sha = (C.c_uint8 * 32)()
+    _check(L.lib().tsf_snapshot_write(
+        os.fsencode(path), system.natoms, _ptr(system.positions), _ptr(system.species), ns,
+        _ptr(m), _ptr(system.box.lengths), _ptr(system.box.periodic),
+        _ptr(system.velocities) if velocities else None, flags, sha))
+    return bytes(sha).hex()
+
+
+def snapshot_info(path: str) -> dict:
+    """Header of a snapshot after its checksum is verified."""
+    n, ns, fl = C.c_int64(), C.c_int(), C.c_uint32()
+    sha = (C.c_uint8 * 32)()
+    _check(L.lib().tsf_snapshot_info(os.fsencode(path), C.byref(n), C.byref(ns), C.byref(fl),
+                                     sha))
+    return {"natoms": n.value, "species_count": ns.value, "flags": fl.value,
+            "sha256": bytes(sha).hex()}
+
+
+def load_snapshot(path: str) -> AtomSystem:
+    """Read a snapshot (checksum verified) into an AtomSystem."""
+    info = snapshot_info(path)
+    n, ns = info["natoms"], info["species_count"]
+    xyz, vel = np.zeros((n, 3)), np.zeros((n, 3))
+    sp = np.zeros(n, np.int32)
+    m, box = np.zeros(ns), np.zeros(3)
+    per = np.zeros(3, np.uint8)
+    _check(L.lib().tsf_snapshot_read(os.fsencode(path), _ptr(xyz), _ptr(sp), _ptr(m), _ptr(box),
+                                     _ptr(per), _ptr(vel)))
+    return AtomSystem(xyz, vel, species=sp, species_masses=list(m),
+                      box=SimulationBox(*box, *(bool(p) for p in per)))
+
+
+# --------------------------------------------------------------------------
 # device context
 # --------------------------------------------------------------------------
 PRECISIONS = {"ref": 0, "opt-d": 0, "double": 0, "opt-m": 1, "mixed": 1, "opt-s": 2, "single": 2}

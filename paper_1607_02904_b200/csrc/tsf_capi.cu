@@ -29,6 +29,15 @@ void perturbed_lattice(const Params& p, int cells, double jitter, std::uint64_t 
                        double* xyz, std::int32_t* species, double* masses, double* box);
 void maxwell_boltzmann(std::int64_t n, const std::int32_t* species, const double* masses,
                        double temperature, std::uint64_t seed, double* v);
+// On-disk snapshots (tsf_snapshot.cpp).
+void snapshot_write(const char* path, std::int64_t n, const double* xyz,
+                    const std::int32_t* species, int ns, const double* masses, const double* box,
+                    const std::uint8_t* periodic, const double* vel, std::uint32_t flags,
+                    std::uint8_t* sha_out);
+void snapshot_info(const char* path, std::int64_t* n, int* ns, std::uint32_t* flags,
+                   std::uint8_t* sha_out);
+void snapshot_read(const char* path, double* xyz, std::int32_t* species, double* masses,
+                   double* box, std::uint8_t* periodic, double* vel);
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -165,6 +174,7 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.n_energy = -1;
     c.n_interior = -1;
     c.split_slots = -1;
+    c.center_slots = -1;
     ++c.list_version;
     c.npad = int(std::max<std::int64_t>(32, (n + 31) / 32 * 32));
     const std::size_t nn = std::size_t(std::max<std::int64_t>(n, 1));
@@ -490,6 +500,26 @@ int tsf_init_velocities(int64_t n, const int32_t* species, const double* masses,
                [&] { tsf::maxwell_boltzmann(n, species, masses, temperature, seed, vel); });
 }
 
+/* ---- snapshots ---- */
+int tsf_snapshot_write(const char* path, int64_t n, const double* xyz, const int32_t* species,
+                       int nspecies, const double* masses, const double box[3],
+                       const uint8_t periodic[3], const double* vel, uint32_t flags,
+                       uint8_t sha256_out[32]) {
+  return guard(nullptr, [&] {
+    tsf::snapshot_write(path, n, xyz, species, nspecies, masses, box, periodic, vel, flags,
+                        sha256_out);
+  });
+}
+int tsf_snapshot_info(const char* path, int64_t* n, int* nspecies, uint32_t* flags,
+                      uint8_t sha256_out[32]) {
+  return guard(nullptr, [&] { tsf::snapshot_info(path, n, nspecies, flags, sha256_out); });
+}
+int tsf_snapshot_read(const char* path, double* xyz, int32_t* species, double* masses,
+                      double box[3], uint8_t periodic[3], double* vel) {
+  return guard(nullptr,
+               [&] { tsf::snapshot_read(path, xyz, species, masses, box, periodic, vel); });
+}
+
 /* ---- context ---- */
 int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
   *out = nullptr;
@@ -707,11 +737,50 @@ int tsf_build_neighbor_list(tsf_ctx* ctx, double cutoff, double skin) {
   return guard(&ctx->c, [&] { tsf::list_build(ctx->c, cutoff, skin); });
 }
 
+// Identity of an adopted list: a 4-lane multiply-xor hash over every word
+// of (n, cutoff, skin, offsets, neighbors) — ~30 GB/s on the host, so the
+// drop-in shim's per-call adoption of the same NeighborList (Engine::run
+// passes it every step, engine.cpp:136-140) costs a scan instead of the
+// CSR -> ELL conversion, the upload and a new graph key.
+std::uint64_t list_identity(std::int64_t n, const int32_t* offsets, const int32_t* nbrs,
+                            double cutoff, double skin) {
+  constexpr std::uint64_t kMul = 0x9E3779B97F4A7C15ull;
+  std::uint64_t h[4] = {std::uint64_t(n) ^ 0x243F6A8885A308D3ull, 0x13198A2E03707344ull,
+                        0xA4093822299F31D0ull, 0x082EFA98EC4E6C89ull};
+  std::uint64_t cb, sb;
+  std::memcpy(&cb, &cutoff, 8);
+  std::memcpy(&sb, &skin, 8);
+  h[1] ^= cb;
+  h[2] ^= sb;
+  auto mix = [&](const int32_t* p, std::int64_t len) {
+    std::int64_t i = 0;
+    for (; i + 8 <= len; i += 8)
+      for (int l = 0; l < 4; ++l) {
+        std::uint64_t w;
+        std::memcpy(&w, p + i + 2 * l, 8);
+        h[l] = (h[l] ^ w) * kMul;
+        h[l] ^= h[l] >> 29;
+      }
+    for (; i < len; ++i) h[0] = ((h[0] ^ std::uint32_t(p[i])) * kMul) ^ (h[0] >> 31);
+  };
+  mix(offsets, n + 1);
+  mix(nbrs, offsets[n]);
+  std::uint64_t r = h[0];
+  for (int l = 1; l < 4; ++l) r = (r ^ (h[l] + kMul + (r << 6) + (r >> 2))) * kMul;
+  return r ^ (r >> 32);
+}
+
 int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* nbrs,
                           double cutoff, double skin) {
   return guard(&ctx->c, [&] {
     Ctx& c = ctx->c;
     if (offsets[0] != 0) throw tsf::ConfigError("neighbor offsets must start at 0");
+    const std::uint64_t id = list_identity(c.n, offsets, nbrs, cutoff, skin);
+    if (c.adopted_valid && c.adopted_id == id && c.skin_list.valid && !c.sorted) {
+      ++c.adoption_hits;   // the list already on the device: keep it, its graphs
+      return;              // and its reference positions
+    }
+    c.adopted_valid = false;
     tsf::unsort(c);  // an external list speaks user indices: slot == user index
     c.short_list.valid = false;
     c.tiled = false;
@@ -737,18 +806,24 @@ int tsf_set_neighbor_list(tsf_ctx* ctx, const int32_t* offsets, const int32_t* n
     c.skin_list.cap = cap;
     c.skin_list.nbr.reserve(ell.size());
     c.skin_list.cnt.reserve(cnt.size());
-    TSF_CUDA(cudaMemcpy(c.skin_list.nbr.get(), ell.data(), sizeof(int) * ell.size(),
-                        cudaMemcpyHostToDevice));
-    TSF_CUDA(cudaMemcpy(c.skin_list.cnt.get(), cnt.data(), sizeof(int) * cnt.size(),
-                        cudaMemcpyHostToDevice));
+    // ordered on the context's stream (a filter may still read the old list)
+    // and complete before the pageable host vectors go out of scope
+    TSF_CUDA(cudaMemcpyAsync(c.skin_list.nbr.get(), ell.data(), sizeof(int) * ell.size(),
+                             cudaMemcpyHostToDevice, c.stream));
+    TSF_CUDA(cudaMemcpyAsync(c.skin_list.cnt.get(), cnt.data(), sizeof(int) * cnt.size(),
+                             cudaMemcpyHostToDevice, c.stream));
+    TSF_CUDA(cudaStreamSynchronize(c.stream));
     c.skin_list.max_count = mx;
     c.skin_list.valid = true;
     c.cutoff = cutoff;
     c.skin = skin;
     c.short_max_stale = true;
     c.split_slots = -1;          // an external list: slots follow user order
+    c.center_slots = -1;
     ++c.list_version;
     tsf::snapshot_reference_positions(c);
+    c.adopted_id = id;
+    c.adopted_valid = true;
   });
 }
 
@@ -762,8 +837,11 @@ int64_t tsf_neighbor_entries(tsf_ctx* ctx, int which) {
     Ctx& c = ctx->c;
     const tsf::ListState& s = list_for(c, which);
     std::vector<int> cnt(std::size_t(c.n));
-    if (c.n > 0)
-      TSF_CUDA(cudaMemcpy(cnt.data(), s.cnt.get(), sizeof(int) * c.n, cudaMemcpyDeviceToHost));
+    if (c.n > 0) {
+      TSF_CUDA(cudaMemcpyAsync(cnt.data(), s.cnt.get(), sizeof(int) * c.n,
+                               cudaMemcpyDeviceToHost, c.stream));
+      TSF_CUDA(cudaStreamSynchronize(c.stream));
+    }
     total = 0;
     for (int v : cnt) total += v;
   });
@@ -780,7 +858,9 @@ int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbr
     // (neighbor.cpp:114; the filter keeps that order, neighbor.cpp:143-152)
     std::vector<int> perm(std::size_t(c.n)), slot_of(std::size_t(c.n));
     if (c.sorted && c.n > 0) {
-      TSF_CUDA(cudaMemcpy(perm.data(), c.perm.get(), sizeof(int) * c.n, cudaMemcpyDeviceToHost));
+      TSF_CUDA(cudaMemcpyAsync(perm.data(), c.perm.get(), sizeof(int) * c.n,
+                               cudaMemcpyDeviceToHost, c.stream));
+      TSF_CUDA(cudaStreamSynchronize(c.stream));
     } else {
       for (std::int64_t q = 0; q < c.n; ++q) perm[std::size_t(q)] = int(q);
     }

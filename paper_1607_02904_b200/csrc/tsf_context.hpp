@@ -175,6 +175,10 @@ struct Ctx {
   // CUDA graph of the steady-state evaluation (filter + force launches),
   // replayed while its key holds; see evaluate() in tsf_capi.cu
   std::uint64_t list_version = 0;      // bumped by every list / centre-set change
+  // identity of the externally supplied list on the device (tsf_set_neighbor_list)
+  std::uint64_t adopted_id = 0;
+  bool adopted_valid = false;          // cleared by every device-side list build
+  std::int64_t adoption_hits = 0;      // adoptions that found the same list resident
   // (slot 0: a whole evaluation; 1 and 2: the two phases of a split one)
   struct GraphSlot {
     cudaGraphExec_t exec = nullptr;

@@ -881,7 +881,16 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.ns = c.params.species_count();
   a.flags = c.flags.get();
   c.overflow.reserve(std::max<std::size_t>(3 * n, 1));
-  c.partials.reserve(std::size_t(32 * 148 + 4 * kOverflowBlocks + 8) * kRedWidth);
+  {
+    // one partial row per block: two phases' main launches (each at most
+    // resident-blocks-per-SM x SMs, persistent_blocks), up to three tier
+    // launches plus k_queued_ev of kOverflowBlocks each
+    int dev = 0, sms = 148;
+    TSF_CUDA(cudaGetDevice(&dev));
+    TSF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const std::size_t max_main = std::size_t(sms) * (2048 / kBlock);
+    c.partials.reserve((2 * max_main + 4 * kOverflowBlocks + 8) * kRedWidth);
+  }
   a.partials = c.partials.get();
   if (c.phase_first && !(flags & kFlagFlagsZeroed))
     TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 4 * sizeof(int), c.stream));

@@ -558,6 +558,19 @@ PairBounds pair_bounds(const Ctx& c, FilterMode mode) {
         pb.c2[i * ns + k] = c2;
         pb.cut[i * ns + k] = cut;
       }
+    // Symmetric bounds: the deterministic scatter has atom a collect the
+    // force slots of the centres in its OWN short list (k_gather), so k must
+    // list i whenever i lists k.  A LAMMPS-format table may give (i,*,k) and
+    // (k,*,i) different R/D; the larger bound only adds entries whose terms
+    // are exact zeros (outside every cutoff of their rows).
+    if (mode == FilterMode::Pair)
+      for (int i = 0; i < ns; ++i)
+        for (int k = i + 1; k < ns; ++k) {
+          const double c2 = std::max(pb.c2[i * ns + k], pb.c2[k * ns + i]);
+          const double cut = std::max(pb.cut[i * ns + k], pb.cut[k * ns + i]);
+          pb.c2[i * ns + k] = pb.c2[k * ns + i] = c2;
+          pb.cut[i * ns + k] = pb.cut[k * ns + i] = cut;
+        }
   } else {
     pb.ns = 1;
   }
@@ -750,6 +763,7 @@ void list_build(Ctx& c, double cutoff, double skin) {
     if (mx <= cap) {
       c.skin_list.cap = cap;
       c.skin_list.valid = true;
+      c.adopted_valid = false;
       // the filter requests 4 near_pre entries of a near list up front: the
       // fewest blocks that leave at most 1/256 of the atoms to the serial tail
       const int tail = n / 256;

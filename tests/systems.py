@@ -123,3 +123,35 @@ def lammps_style(text):
             line = " ".join(t)
         out.append(line)
     return "\n".join(out) + "\n"
+
+
+# ---- BASELINE.json configurations at their full sizes -------
+LIQUID_SNAPSHOT = "liquid512k.tsfsnap"      # under tests/golden (tools/make_liquid_snapshot.py)
+
+
+def baseline_cfg4(tb, cells=(80, 80, 40)):
+    """cfg 4 as bench.py times it: Si diamond 80x80x40 = 2,048,000 atoms with a
+    seeded uniform +-0.15 A jitter (seed 12345), wrapped into the box; skin 1."""
+    s = tb.make_diamond_lattice(*cells, 5.431)
+    rng = np.random.default_rng(12345)
+    xyz = _wrap(s.positions + rng.uniform(-0.15, 0.15, s.positions.shape), s.box.lengths)
+    return Case("cfg4_si2m", xyz, s.species, s.box.lengths, s.box.periodic, 1.0, si_text(tb))
+
+
+def baseline_cfg3(tb, sic_text):
+    """cfg 3 as bench.py times it: 3C-SiC 32^3 cells = 262,144 atoms at
+    a0 = 4.32, +-0.10 A jitter (seed 12345)."""
+    c = zincblende(tb, sic_text, 32, a0=4.32, jitter=0.10, seed=12345, skin=1.0)
+    c.name = "cfg3_sic262k"
+    return c
+
+
+def baseline_cfg5(golden_dir):
+    """cfg 5: the committed liquid-Si snapshot (512,000 atoms, 3000 K), read by
+    the independent numpy reader so the oracle side never loads the product."""
+    import os
+    from oracle import snapshot as osnap
+    from oracle.oracle import SI_TEXT
+    d = osnap.read(os.path.join(golden_dir, LIQUID_SNAPSHOT))
+    return Case("cfg5_liquid512k", d["positions"], d["species"], d["box"], d["periodic"], 1.0,
+                SI_TEXT)

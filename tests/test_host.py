@@ -184,3 +184,72 @@ def test_bench_algorithmic_work_counter(tb, oracle):
                 Tb += sum(1 for k in seg if k != j and
                           r2(i, k) <= op.rows[(si * op.ns + sj) * op.ns + c.species[k], 15])
         assert (P, T) == (Pb, Tb)
+
+
+def test_snapshot_round_trip(tb, sic_text, tmp_path):
+    """TSFSNAP1 (csrc/tsf_snapshot.cpp): the product's writer and reader, the
+    independent numpy reader (oracle/snapshot.py) and hashlib agree; float64
+    coordinates round-trip bit for bit, float32 ones as the float32 rounding."""
+    import hashlib
+    from oracle import snapshot as osnap
+    params = tb.parse_params(sic_text)
+    s = tb.perturbed_lattice(params, 3, 0.2, 7)
+    tb.init_velocities(s, 900.0, 5)
+    for f32, vel in [(False, False), (False, True), (True, False), (True, True)]:
+        path = str(tmp_path / f"s_{int(f32)}{int(vel)}.tsfsnap")
+        sha = tb.save_snapshot(path, s, float32_coords=f32, velocities=vel)
+        raw = open(path, "rb").read()
+        assert hashlib.sha256(raw[:-32]).hexdigest() == sha == raw[-32:].hex()
+        info = tb.snapshot_info(path)
+        assert info["natoms"] == s.natoms and info["species_count"] == 2
+        assert info["sha256"] == sha
+        back = tb.load_snapshot(path)
+        ref = osnap.read(path)
+        want = s.positions.astype(np.float32).astype(np.float64) if f32 else s.positions
+        assert np.array_equal(back.positions, want) and np.array_equal(ref["positions"], want)
+        assert np.array_equal(back.species, s.species) and np.array_equal(ref["species"],
+                                                                            s.species)
+        assert back.species_masses == list(s.species_masses)
+        assert np.array_equal(back.box.lengths, s.box.lengths)
+        assert np.array_equal(ref["box"], s.box.lengths)
+        assert np.array_equal(back.box.periodic, s.box.periodic)
+        if vel:
+            assert np.array_equal(back.velocities, s.velocities)
+            assert np.array_equal(ref["velocities"], s.velocities)
+        else:
+            assert not back.velocities.any() and ref["velocities"] is None
+    # a flipped byte anywhere fails the checksum in both readers
+    bad = bytearray(open(path, "rb").read())
+    bad[100] ^= 1
+    badp = str(tmp_path / "bad.tsfsnap")
+    open(badp, "wb").write(bytes(bad))
+    with pytest.raises(tb.ConfigError, match="SHA-256"):
+        tb.load_snapshot(badp)
+    with pytest.raises(ValueError, match="SHA-256"):
+        osnap.read(badp)
+    with pytest.raises(tb.ConfigError, match="cannot open"):
+        tb.load_snapshot(str(tmp_path / "missing.tsfsnap"))
+    s.species[3] = 5
+    with pytest.raises(tb.ConfigError, match="species id"):
+        tb.save_snapshot(str(tmp_path / "x.tsfsnap"), s)
+
+
+def test_bench_reference_arm_inputs_without_product(tb, reference):
+    """bench.py --impl reference builds the workload through the reference's own
+    generator (oracle/_ref) and never loads the product; its arrays equal the
+    GPU arm's (bench.make_system) bit for bit."""
+    import subprocess
+    import sys
+    import bench
+    from oracle.oracle import Reference
+    for cfg in ("si32k", "sic256k"):
+        a = bench.make_system(cfg)
+        b = bench.make_system_reference(cfg, Reference())
+        for x, y in zip(a[1:5], b[1:5]):
+            assert np.array_equal(np.asarray(x), np.asarray(y)), cfg
+        assert a[5] == b[5]
+        assert tb.parse_params(a[0]).serialize() == tb.parse_params(b[0]).serialize()
+    code = ("import sys, bench; from oracle.oracle import Reference; "
+            "bench.make_system_reference('si32k', Reference()); "
+            "assert not [m for m in sys.modules if m.startswith('paper_1607_02904_b200')]")
+    subprocess.run([sys.executable, "-c", code], cwd=ROOT, check=True)

@@ -182,3 +182,24 @@ def test_virial_is_strain_derivative(tb, oracle):
 def test_compensated_energy_tracks_naive(tb, oracle):
     *_, ref = run_oracle(oracle, systems.perturbed(tb, 4, 0.12, 32, 0.5))
     assert abs(ref["energy"] - ref["energy_ld"]) <= 1e-13 * abs(ref["energy"])
+
+
+def test_cfg2_nve_golden(reference):
+    """SURVEY.md 8d cfg 2: the reference Engine (ref scheme, 1 thread) on
+    20x20x10 cells at 1600 K, seed 12345, dt 1 fs, skin 1, 100 steps gives
+    Etot0 / Etot100 / rebuilds — the golden test_gpu_scale.py holds the GPU
+    engine to (bitwise here: this glibc and these compile flags)."""
+    from oracle.oracle import SI_TEXT
+    from test_gpu_scale import CFG2_ETOT0, CFG2_ETOT100, CFG2_REBUILDS
+    R = reference
+    h = R.diamond_lattice(20, 20, 10)
+    R.init_velocities(h, 1600.0, 12345)
+    ph = R.params(SI_TEXT)
+    rep = R.run_nve(h, ph, 100, dt=0.001, skin=1.0, scheme="ref", precision="ref",
+                    thermo_every=10)
+    assert rep["etot_first"] == CFG2_ETOT0
+    assert rep["etot_last"] == CFG2_ETOT100
+    assert rep["rebuilds"] == CFG2_REBUILDS
+    R.free_system(rep["final"])
+    R.free_system(h)
+    R.free_params(ph)
