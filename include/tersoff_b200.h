@@ -144,6 +144,14 @@ int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xy
                         double skin, uint32_t flags, double* energy, double* forces,
                         double* virial);
 
+/* Diagnostics: the device math on n host values x (current device), out[2n]:
+ * fn 0 exp (constant-bank polynomial), 1 log (same), 2 libdevice exp, 3
+ * libdevice log (out[2q] = f(x[q])); 4 bond order b, db/dzeta at zeta = x[q]
+ * in double, 5 in float, 6 the reference's pow form in double (row (0,0,0)
+ * of p; out[2q] = b, out[2q+1] = db); 7 the double bond order's path at
+ * zeta = x[q] (out[2q] = 1 for the series, out[2q+1] = ln u). */
+int tsf_math_probe(const tsf_params* p, int fn, int64_t n, const double* x, double* out);
+
 /* Kernel launches issued by this context since creation (evidence counter). */
 int64_t tsf_launch_count(const tsf_ctx* ctx);
 

@@ -82,6 +82,7 @@ PROTOTYPES = [
     ("tsf_compute_f32", C.c_int, [_vp, C.c_uint32, _vp, _vp, _vp]),
     ("tsf_evaluate_forces", C.c_int, [_vp, C.c_int, C.c_int64, _vp, _vp, _vp, _vp, _d,
                                       C.c_uint32, _vp, _vp, _vp]),
+    ("tsf_math_probe", C.c_int, [_vp, C.c_int, C.c_int64, _vp, _vp]),
     ("tsf_launch_count", C.c_int64, [_vp]),
     ("tsf_profile_enable", C.c_int, [_vp, C.c_int]),
     ("tsf_profile_read", C.c_int, [_vp, _vp, _i64p, C.c_int]),

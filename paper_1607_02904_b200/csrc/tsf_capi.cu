@@ -29,6 +29,8 @@ void perturbed_lattice(const Params& p, int cells, double jitter, std::uint64_t 
                        double* xyz, std::int32_t* species, double* masses, double* box);
 void maxwell_boltzmann(std::int64_t n, const std::int32_t* species, const double* masses,
                        double temperature, std::uint64_t seed, double* v);
+// Device math diagnostics (tsf_force.cu).
+void math_probe(const Params& p, int fn, std::int64_t n, const double* x, double* out);
 // On-disk snapshots (tsf_snapshot.cpp).
 void snapshot_write(const char* path, std::int64_t n, const double* xyz,
                     const std::int32_t* species, int ns, const double* masses, const double* box,
@@ -498,6 +500,11 @@ int tsf_init_velocities(int64_t n, const int32_t* species, const double* masses,
                         double temperature, uint64_t seed, double* vel) {
   return guard(nullptr,
                [&] { tsf::maxwell_boltzmann(n, species, masses, temperature, seed, vel); });
+}
+
+/* ---- diagnostics ---- */
+int tsf_math_probe(const tsf_params* p, int fn, int64_t n, const double* x, double* out) {
+  return guard(nullptr, [&] { tsf::math_probe(p->p, fn, n, x, out); });
 }
 
 /* ---- snapshots ---- */

@@ -708,6 +708,9 @@ Row<R> make_row(const Entry& e) {
   r.rpd = R(e.big_r + e.big_d);
   r.nqd = R(-pi / 4 / e.big_d);
   const double c2 = e.c * e.c, d2 = e.d * e.d;
+  // bond-order series path (tsf_math.cuh): u < 2^-12 and |u / (2 eta)| < 2^-8
+  r.lnu_fast = R(e.eta > 0 ? std::min(std::log(0x1p-12), std::log(0x1p-8 * 2.0 * e.eta))
+                           : -1e300);
   r.gamma = R(e.gamma);
   r.gcd2 = R(e.gamma * c2 / d2);
   r.gc2 = R(e.gamma * c2);
