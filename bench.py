@@ -301,6 +301,43 @@ def cpu_baseline(text, xyz, species, box, per, masses):
             "sample": f"compute_ref (1 thread) on the full {n}-atom system, one call, {t:.2f} s"}
 
 
+def md_leg(tb, params, args):
+    """NVE MD steps through tsf_md_run on the workload's lattice at 1600 K
+    (init_velocities seed 12345, dt 1 fs, skin 1 A, thermo every 100 steps):
+    W warm-up steps, then max(100, K) timed steps including every rebuild."""
+    import torch
+    cells = CONFIGS[args.config][0]
+    s = tb.make_diamond_lattice(*cells, CONFIGS[args.config][1])
+    tb.init_velocities(s, 1600.0, 12345)
+    ctx = tb.Context(params, 0)
+    ctx.load(s)
+    ctx.build_neighbor_list(params.r_cut_max, 1.0)
+    ctx.md_set_state(s.velocities, s.species_masses)
+    det = args.deterministic
+    ctx.md_run(max(args.warmup, 20), 0.001, args.precision, det, 100)
+    steps = max(100, args.steps)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.cuda.current_device())
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    thermo, rebuilds = ctx.md_run(steps, 0.001, args.precision, det, 100)
+    e1.record(stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    etot = thermo[:, 1] + thermo[:, 2]
+    ctx.close()
+    n = s.natoms
+    return {"metric": "MD atom-steps/s", "value": n * steps / t, "unit": UNIT,
+            "ms_per_step": 1e3 * t / steps, "steps": steps, "rebuilds": int(rebuilds),
+            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": args.precision,
+            "scatter": "deterministic gather" if det else "atomics",
+            "workload": f"{CONFIGS[args.config][4]}, perfect lattice + init_velocities(1600 K, "
+                        "seed 12345), dt 1 fs, skin 1 A, needs_rebuild every step, thermo "
+                        "every 100 steps (tsf_md_run)",
+            "rel_energy_drift": float(np.abs(etot - etot[0]).max() / abs(etot[0]))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -313,6 +350,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-md", action="store_true")
     # the multi-GPU code path (GpuEngine + Decomposition) on one rank: a smoke
     # test of bench's N>1 branch where only one GPU is available
     ap.add_argument("--decompose", action="store_true")
@@ -535,6 +573,14 @@ def main():
                               "dtype": DTYPES[prec], "kernel_ms": kms, "force_stage_ms": sms,
                               "roofline_frac": algo_flop / (sms * 1e-3) / 1e12 / vpeak}
 
+    # MD-step leg (the paper's timing; Engine::run,
+    # engine.cpp:174-199): GPU-resident velocity Verlet on cfg 4 at 1600 K —
+    # kick, drift, the needs_rebuild test every step, list rebuilds, the
+    # evaluation — timed with CUDA events on the context's stream
+    md = None
+    if world == 1 and not args.no_md and args.config in ("si2m", "si32k"):
+        md = md_leg(tb, params, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(text, xyz, species, box, per, masses)
@@ -574,6 +620,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "md": md,
             "variants": variants,
             "gpu_launches": launches,
             "clocks": clk,

@@ -228,9 +228,13 @@ void download_forces(Ctx& c, double* forces) {
 }
 
 void raise_device_errors(Ctx& c) {
-  int f[8] = {0};
+  int f[24] = {0};
   TSF_CUDA(cudaMemcpyAsync(f, c.flags.get(), sizeof f, cudaMemcpyDeviceToHost, c.stream));
   TSF_CUDA(cudaStreamSynchronize(c.stream));
+  if (f[tsf::kFlagFilterNaN]) {
+    TSF_CUDA(cudaMemsetAsync(c.flags.get() + tsf::kFlagFilterNaN, 0, sizeof(int), c.stream));
+    throw tsf::NumericError("non-finite pair term (a coordinate is NaN)");
+  }
   if (f[7] & tsf::kErrBadSpecies) {
     TSF_CUDA(cudaMemsetAsync(c.flags.get() + 7, 0, sizeof(int), c.stream));
     c.host_species.clear();
@@ -384,7 +388,8 @@ void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
         "no neighbor list: call tsf_build_neighbor_list or tsf_set_neighbor_list first");
   const int mode = int((flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
   const bool steady = !c.short_max_stale && c.short_apply == mode;
-  const std::uint64_t key[6] = {c.list_version, std::uint64_t(p), flags, std::uint64_t(c.n),
+  const std::uint64_t key[6] = {c.list_version, std::uint64_t(p),
+                                flags | (c.speculative ? 0x80000000u : 0u), std::uint64_t(c.n),
                                 std::uint64_t(c.n_owned),
                                 std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
   const bool graphable = graphs_enabled() && !c.graphs_off && !c.profile && steady && c.n > 0;
@@ -566,6 +571,8 @@ void tsf_destroy(tsf_ctx* ctx) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.pinned) cudaFreeHost(c.pinned);
   c.pinned = nullptr;
+  if (c.pinned_flag) cudaFreeHost(c.pinned_flag);
+  if (c.flag_event) cudaEventDestroy(c.flag_event);
   for (auto& g : c.graph)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& e : c.ev)
@@ -967,7 +974,7 @@ int tsf_md_kick(tsf_ctx* ctx, double dt, int drift, int kicks, int* moved) {
     if (moved) {
       int f = 0;
       if (check)
-        TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost,
+        TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + tsf::kFlagMoved, sizeof(int), cudaMemcpyDeviceToHost,
                                  c.stream));
       TSF_CUDA(cudaStreamSynchronize(c.stream));
       *moved = check ? f : 1;   // no list: a build is due anyway
@@ -1021,19 +1028,41 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
     // velocity Verlet (engine.cpp:142-172).  The closing half-kick of a step
     // is deferred into the next step's opening kick + drift (one pass over
     // the atoms instead of two) unless a sample needs full-step velocities.
+    // Speculative: the evaluation is queued behind the kick before the host
+    // knows the kick's needs_rebuild result; only the 4-byte flag is awaited
+    // (an event right after the kick), so the GPU runs step s's evaluation
+    // while the host decides and queues step s+1.  A stale list (a rebuild
+    // step, every ~20 steps at 1600 K) makes that evaluation's launches return
+    // at once; the step is then rebuilt and evaluated again — the reference's
+    // rebuild schedule and results (neighbor.cpp:134-141, engine.cpp:174-199).
+    if (!c.pinned_flag)
+      TSF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c.pinned_flag), 64,
+                             cudaHostAllocDefault));
+    if (!c.flag_event) TSF_CUDA(cudaEventCreateWithFlags(&c.flag_event, cudaEventDisableTiming));
+    struct Spec {
+      Ctx& c;
+      explicit Spec(Ctx& cc) : c(cc) { c.speculative = !c.profile; }
+      ~Spec() { c.speculative = false; }
+    } spec(c);
     bool kick_pending = false;
     for (std::int64_t s = 1; s <= steps; ++s) {
-      // kick + drift + the rebuild test in one pass; only its flag comes back
+      // kick + drift + the rebuild test in one pass (flags[kFlagMoved])
       tsf::md_kick(c, dt, true, kick_pending ? 2 : 1, /*check_rebuild=*/true);
-      int moved = 0;
-      TSF_CUDA(cudaMemcpyAsync(&moved, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost,
-                               c.stream));
-      TSF_CUDA(cudaStreamSynchronize(c.stream));
-      if (moved) {
+      TSF_CUDA(cudaMemcpyAsync(c.pinned_flag, c.flags.get() + tsf::kFlagMoved, sizeof(int),
+                               cudaMemcpyDeviceToHost, c.stream));
+      TSF_CUDA(cudaEventRecord(c.flag_event, c.stream));
+      if (c.speculative) evaluate(c, p, flags);
+      TSF_CUDA(cudaEventSynchronize(c.flag_event));
+      if (*c.pinned_flag) {
+        // the speculative launches saw the flag and returned; clear it
+        // behind them so the re-evaluation runs
+        TSF_CUDA(cudaMemsetAsync(c.flags.get() + tsf::kFlagMoved, 0, sizeof(int), c.stream));
         tsf::list_build(c, c.cutoff, c.skin);
         ++nreb;
+        evaluate(c, p, flags);
+      } else if (!c.speculative) {
+        evaluate(c, p, flags);
       }
-      evaluate(c, p, flags);
       if (s % thermo_every == 0 || s == steps) {
         tsf::md_kick(c, dt, false);
         sample(s);

@@ -63,6 +63,16 @@ void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t stre
 
 // Per-step reduction slots (energy + 6 virial components) per block.
 constexpr int kRedWidth = 8;
+// flags[] words outside the force path's [0..17]: the needs_rebuild result of
+// the position writers (kick, k_needs_rebuild) — its own word, so the
+// filter's per-evaluation zeroing of [0..3] cannot race a speculative
+// readback (tsf_md_run) — and a word that stays zero (the "skip" pointer of
+// non-speculative evaluations)
+constexpr int kFlagMoved = 18;
+constexpr int kFlagZero = 19;
+// NaN distances seen by a force-path filter (its own word: the filter's block 0
+// zeroes flags[0..3] while other blocks run); cleared when raised
+constexpr int kFlagFilterNaN = 20;
 
 struct ListState {
   int cap = 0;                 // ELL slots per atom
@@ -175,6 +185,13 @@ struct Ctx {
   // CUDA graph of the steady-state evaluation (filter + force launches),
   // replayed while its key holds; see evaluate() in tsf_capi.cu
   std::uint64_t list_version = 0;      // bumped by every list / centre-set change
+  // tsf_md_run's speculative step: the evaluation is queued behind the kick
+  // before its rebuild flag is known; its filter and force launches return at
+  // once when flags[kFlagMoved] is set (the step is then re-evaluated after
+  // the rebuild), so the GPU never waits for the host between steps
+  bool speculative = false;
+  int* pinned_flag = nullptr;          // page-locked host word for the flag readback
+  cudaEvent_t flag_event = nullptr;
   // identity of the externally supplied list on the device (tsf_set_neighbor_list)
   std::uint64_t adopted_id = 0;
   bool adopted_valid = false;          // cleared by every device-side list build

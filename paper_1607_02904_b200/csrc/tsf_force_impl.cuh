@@ -82,9 +82,19 @@ struct ForceArgs {
   int* ovf_out_count;
   double* atom_ev;          // deterministic tiers: per-atom energy + virial [n][8]
   int* flags;               // [0] error bits
+  const int* skip;          // speculative MD step: return at once when *skip != 0
 };
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Which exponentials use the branch-free constant-bank exp (tsf_math.cuh
+// exp_cb, Estrin) instead of libdevice's: 0 none, 1 the triplet's, 2 also the
+// pair terms'.  Measured (tools/ab.py, si2m f64 kernel): 0 0.320 ms, 1 0.344,
+// 2 0.345 — libdevice's exp (one integer scale, a rarely taken range branch)
+// beats the branch-free two-factor form despite the ILP the latter allows.
+#ifndef TSF_EXP_FIN
+#define TSF_EXP_FIN 0
+#endif
 
 // Parameter-table specialisations.
 enum Spec : int {
@@ -161,7 +171,11 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
   const R dg = R(-2) * p.gc2 * t * iden * iden;
   const R arg = ok ? p.lam3 * (j.r - k.r) : R(0);
   const bool cubic = p.m3 != R(0);
+#if TSF_EXP_FIN >= 1
+  const R ex = Fn<R>::exp_fin(cubic ? arg * arg * arg : arg);
+#else
   const R ex = Fn<R>::exp_(cubic ? arg * arg * arg : arg);
+#endif
   const R gx = g * ex;
   o.z = fck * gx;
   const R fge = o.z * (cubic ? R(3) * p.lam3 * (arg * arg) : p.lam3);   // dz/dr_ij via exp
@@ -231,6 +245,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
 
   griddep_wait();     // launch_pdl: the previous launch has completed
   griddep_launch();
+  if (a.skip && *a.skip) return;   // a speculative step whose list went stale
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   Acc e_acc = 0;
@@ -391,8 +406,13 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     cutoff_ramp(me.r, pjj, fc, dfc);
     // the radial pair terms depend on r only: issued before the zeta pass so
     // their two exp chains overlap it instead of lengthening the pair block
+#if TSF_EXP_FIN >= 2
+    const R fr = pjj.a * Fn<R>::exp_fin(-pjj.lam1 * me.r);
+    const R fa = -(pjj.b * Fn<R>::exp_fin(-pjj.lam2 * me.r));
+#else
     const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
     const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
+#endif
     // meta: species of this slot as a k, or -1 when it can never be one.
     // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
     // exactly "pair (i, k) inside its own cutoff".
@@ -883,6 +903,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
   a.cutsq = c.cutsq.get();
   a.ns = c.params.species_count();
   a.flags = c.flags.get();
+  a.skip = c.speculative ? c.flags.get() + kFlagMoved : nullptr;
   c.overflow.reserve(std::max<std::size_t>(3 * n, 1));
   {
     // one partial row per block: two phases' main launches (each at most

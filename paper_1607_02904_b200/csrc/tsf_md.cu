@@ -382,11 +382,11 @@ int center_limit(const Ctx& c) {   // user atoms below it are owned (all unless 
 void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
   if (c.n == 0) return;
   const bool check = drift && check_rebuild;
-  if (check) TSF_CUDA(cudaMemsetAsync(c.flags.get() + 2, 0, sizeof(int), c.stream));
+  if (check) TSF_CUDA(cudaMemsetAsync(c.flags.get() + kFlagMoved, 0, sizeof(int), c.stream));
   k_kick<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
       c.pos.get(), c.posf.get(), c.flags.get() + 5, c.vel.get(), c.forces.get(), int(c.n),
       masses_of(c), dt, drift ? 1 : 0, kicks, c.box, c.pos_ref.get(), 0.25 * c.skin * c.skin,
-      check ? c.flags.get() + 2 : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c),
+      check ? c.flags.get() + kFlagMoved : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c),
       disp_ref(c));
   ++c.launches;
 }

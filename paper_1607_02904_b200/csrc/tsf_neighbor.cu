@@ -160,6 +160,7 @@ struct NearIn {
   const int* dmax;   // squared displacement max since the build (float bits)
   float t[2];
   int pre[2];
+  const int* skip;   // speculative MD step: return at once when *skip != 0
 };
 
 // Skin list, one thread per slot: candidates are the stencil cells' slot
@@ -265,6 +266,7 @@ struct FilterBands {
   float lo0, hi0;
   double c20;
   WrapF wrap;
+  int* err;   // flags[0] of a force-path filter (NaN distances), else nullptr
 };
 
 
@@ -322,7 +324,17 @@ __device__ __forceinline__ unsigned resolve_unsure(const ListArgs& a, const Filt
     unsure &= unsure - 1;
     const int b = skin[ell_at(s_base + q, at, a.npad)] & 0x7fffffff;
     const double c2 = MULTI ? fb.c2[(prs >> (4 * q)) & 15] : fb.c20;
-    if (exact_within(a.pos, at, b, a.box, c2)) in |= 1u << q;
+    double dx, dy, dz;
+    displacement(a.pos[at], a.pos[b], a.box, dx, dy, dz);
+    const double r2 = norm_sq_exact(dx, dy, dz);
+    if (r2 <= c2) {
+      in |= 1u << q;
+    } else if (fb.err && r2 != r2) {
+      // a NaN coordinate: the float pre-test sends it here (neither in nor
+      // out); the reference's cutoff tests let the NaN into zeta and throw
+      // NumericError (potential_ref.cpp:109-112) — flag it the same way
+      atomicOr(fb.err + kFlagFilterNaN, 1);
+    }
   }
   return in;
 }
@@ -400,6 +412,7 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     int zero_bytes, int slot_lo, int slot_hi, NearIn near, int* __restrict__ zero_flags) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
+  if (near.skip && *near.skip) return;   // a speculative step whose list went stale
   // error bits and tier queue counts of the force launches that follow
   if (zero_flags && blockIdx.x == 0 && threadIdx.x < 4) zero_flags[threadIdx.x] = 0;
   const int ns = pb.ns;
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
   const int m = Lc[at];
   int w = 0;
   if (apply) {
-    const FilterBands fb{slo, shi, sc2, ns, slo[0], shi[0], sc2[0], wrap_of(a.boxf)};
+    const FilterBands fb{slo, shi, sc2, ns, slo[0], shi[0], sc2[0], wrap_of(a.boxf), zero_flags};
     w = filter_list<MULTI>(a, fb, at, L, m, pre, out);
   } else {
     for (int s = 0; s < m; ++s) out[ell_at(s, at, a.npad)] = skin[ell_at(s, at, a.npad)];
@@ -825,7 +838,9 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
                     {c.near_list[0].cnt.get(), c.near_list[1].cnt.get()},
                     c.flags.get() + 10,
                     {c.near_t[0], c.near_t[1]},
-                    {c.near_pre[0], c.near_pre[1]}};
+                    {c.near_pre[0], c.near_pre[1]},
+                    nullptr};
+    near.skip = c.speculative ? c.flags.get() + kFlagMoved : nullptr;
     (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(std::max(hi - lo, 1)), kBlock, 0,
                                                        c.stream>>>(
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
@@ -852,14 +867,16 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
 
 bool list_needs_rebuild(Ctx& c) {
   if (!c.skin_list.valid) return true;
-  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 2, 0, sizeof(int), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + kFlagMoved, 0, sizeof(int), c.stream));
   if (c.n > 0) {
     k_needs_rebuild<<<blocks_for(c.n), kBlock, 0, c.stream>>>(
-        c.pos.get(), c.pos_ref.get(), int(c.n), c.box, 0.25 * c.skin * c.skin, c.flags.get() + 2);
+        c.pos.get(), c.pos_ref.get(), int(c.n), c.box, 0.25 * c.skin * c.skin,
+        c.flags.get() + kFlagMoved);
     ++c.launches;
   }
   int f = 0;
-  TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + 2, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  TSF_CUDA(cudaMemcpyAsync(&f, c.flags.get() + kFlagMoved, sizeof(int), cudaMemcpyDeviceToHost,
+                           c.stream));
   TSF_CUDA(cudaStreamSynchronize(c.stream));
   return f != 0;
 }
