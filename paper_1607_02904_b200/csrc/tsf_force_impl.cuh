@@ -614,6 +614,12 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   }
 }
 
+}  // namespace
+}  // namespace tsf
+#include "tsf_force_packed.cuh"
+namespace tsf {
+namespace {
+
 // Sum of the block partials in a fixed order.  The partials are read as one
 // flat array: thread t always holds quantity q = t % 8 (1024 % kRedWidth == 0),
 // so every warp load is 256 contiguous bytes; lanes of equal q meet in two
@@ -779,6 +785,29 @@ int launch_main(Ctx& c, ForceArgs<R> a) {
   return blocks;
 }
 
+// read per eager evaluation (graph replays do not come here), so tests can switch them
+int packed_mode() {
+  const char* e = std::getenv("TSF_PACKED");
+  return e ? std::atoi(e) : 1;
+}
+
+int packed_over4_pct() {
+  const char* e = std::getenv("TSF_PACKED_OVER4");
+  return e ? std::atoi(e) : 10;
+}
+
+template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN>
+int launch_main_packed(Ctx& c, ForceArgs<R> a) {
+  const int chunks = std::max(1, ceil_div(a.n_owned - a.slot_base, 32));
+  auto kern = k_force_packed<R, Acc, SPEC, DET, false, FOREIGN>;
+  const int blocks = persistent_blocks(kern, ceil_div(chunks, kBlock / 32));
+  c.mark(2);
+  launch_pdl(kern, blocks, kBlock, c.stream, a);
+  c.mark(3);
+  ++c.launches;
+  return blocks;
+}
+
 template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN>
 void run_force_t(Ctx& c, ForceArgs<R> a) {
   // Group width from the short-count distribution of the last list build
@@ -804,6 +833,15 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   const char* pin = std::getenv("TSF_GROUP_WIDTH");
   const int pinned = pin ? std::atoi(pin) : 0;
   if (pinned == 4 || pinned == 8 || pinned == 16 || pinned == 32) g = pinned;
+  // Packed lane groups (tsf_force_packed.cuh): the tier chain becomes ONE
+  // packed launch over the queue, and an irregular system (over the
+  // TSF_PACKED_OVER4 percent of atoms over 4) runs packed from the start.
+  // TSF_PACKED=0 restores the G-tier chain, 2 forces the packed main launch.
+  const int pmode = packed_mode();
+  const bool packed_main =
+      !(pinned == 4 || pinned == 8 || pinned == 16 || pinned == 32) && pmode >= 1 &&
+      (pmode == 2 || (mx > 4 && s.over4 * 100 > packed_over4_pct() * n));
+  if (packed_main) g = 32;
   // Tier chain: atoms over the main width are queued for G = 8 (when the
   // last rebuild saw counts over 4), then G = 16 (counts over 8), then
   // G = 32, which takes whatever is left — including atoms that outgrew the
@@ -820,11 +858,16 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   // precede this one's; tiers and the reduction run with the last phase
   a.partial_base = c.phase_blocks;
   int nb = c.phase_blocks;
-  switch (g) {
-    case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
-    case 8: nb += launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
-    case 16: nb += launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
-    default: nb += launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
+  if (packed_main) {
+    a.ovf_out = nullptr;
+    nb += launch_main_packed<R, Acc, SPEC, DET, FOREIGN>(c, a);
+  } else {
+    switch (g) {
+      case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
+      case 8: nb += launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
+      case 16: nb += launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
+      default: nb += launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
+    }
   }
   c.phase_blocks = nb;
   if (!c.phase_last) return;
@@ -840,11 +883,19 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     ++c.launches;
     if (!last) ++cur;
   };
-  if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
-  if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
+  if (pmode >= 1) {
+    // one packed launch takes every queued atom, whatever its count
+    if (g < 32)
+      tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN>,
+           mx > g ? kOverflowBlocks : kOverflowBlocks / 4, true);
+  } else {
+    if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
+    if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
+    if (g < 32)
+      tier(k_force<R, Acc, 32, SPEC, DET, true, FOREIGN>,
+           mx > 16 ? kOverflowBlocks : kOverflowBlocks / 4, true);
+  }
   if (g < 32) {
-    tier(k_force<R, Acc, 32, SPEC, DET, true, FOREIGN>,
-         mx > 16 ? kOverflowBlocks : kOverflowBlocks / 4, true);
     if (DET) {
       k_queued_ev<<<kOverflowBlocks, kBlock, 0, c.stream>>>(
           a.atom_ev, a.cnt, a.perm, a.n_owned, a.energy_limit, g, a.flags + 1,

@@ -1,0 +1,390 @@
+// Packed lane groups: the paper's vector repacking (the
+// reference's V2 per-lane traversal, kernels.hpp:304-494) as a warp layout.
+//
+// k_force gives every central atom a power-of-two group of G lanes, so an
+// atom with 5 short neighbours idles 3 lanes of a G = 8 group, and an
+// irregular system (3C-SiC: 45% of the atoms over 4; the 3000 K liquid: 2..13)
+// either idles lanes or queues atoms to wider tier launches.  Here a warp
+// takes a chunk of 32 consecutive atoms (or queued atoms), scans their short
+// counts and packs their neighbour slots back to back: a pack is the longest
+// run of atoms whose slots fit in 32 lanes, segment heads come from a ballot,
+// every lane finds its atom through its segment head, and the rotation scheme
+// of k_force runs inside each segment with its own length n_i (partner
+// k = slot (l + t) mod n_i, stopping at the pack's largest count).  The
+// k-gradients of the first kCacheRot rotations stay in registers; later
+// rotations are recomputed in the scatter pass.  F_i is a segmented sum
+// through shared memory.  Nothing is queued: any count up to 32 is served.
+#pragma once
+
+namespace tsf {
+namespace {
+
+#ifndef TSF_PACKED_SORT
+#define TSF_PACKED_SORT 1
+#endif
+#ifndef TSF_PACKED_CACHE_F64
+#define TSF_PACKED_CACHE_F64 5
+#endif
+#ifndef TSF_PACKED_CACHE_F32
+#define TSF_PACKED_CACHE_F32 7
+#endif
+template <typename R>
+constexpr int kPackedCacheRot =
+    std::is_same<R, double>::value ? TSF_PACKED_CACHE_F64 : TSF_PACKED_CACHE_F32;
+#ifndef TSF_PACKED_MINB_F64
+#define TSF_PACKED_MINB_F64 4
+#endif
+#ifndef TSF_PACKED_MINB_F32
+#define TSF_PACKED_MINB_F32 5
+#endif
+template <typename R>
+constexpr int kPackedMinBlocks =
+    std::is_same<R, double>::value ? TSF_PACKED_MINB_F64 : TSF_PACKED_MINB_F32;
+
+template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN = false>
+__global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
+    k_force_packed(const __grid_constant__ ForceArgs<R> a) {
+  constexpr int kC = kPackedCacheRot<R>;
+  constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
+  __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
+  __shared__ double scut[SPEC == kSingle ? 1 : kRows];
+  __shared__ Stage<R> st;
+  __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
+  __shared__ double s_red[kBlock / 32][kRedWidth];
+  __shared__ int s_atom[kBlock];       // per segment head: slot, count, foreign
+  __shared__ int s_cnt[kBlock];
+  __shared__ int s_fgn[kBlock];
+  __shared__ Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
+
+  griddep_wait();
+  griddep_launch();
+  if (a.skip && *a.skip) return;   // a speculative step whose list went stale
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wbase = tid - lane;
+  Acc e_acc = 0;
+  Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
+
+  const int n_ovf = OVF ? *a.ovf_in_count : 0;
+  if (OVF && n_ovf == 0) {
+    if (tid < kRedWidth)
+      a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
+    return;
+  }
+  const int ns = a.ns;
+  const Row<R>* rows = static_cast<const Row<R>*>(a.rows);
+  const Row<R>& row0 = a.row0;
+  const double cut0 = a.cut0;
+  if (SPEC != kSingle) {
+    for (int q = tid; q < ns * ns * ns; q += blockDim.x) {
+      srow[q] = rows[q];
+      scut[q] = a.cutsq[q];
+    }
+    __syncthreads();
+  }
+  const int last = a.n_all - 1;
+  const bool has_ghosts = a.center_limit < a.n_owned;
+  const bool has_foreign = FOREIGN && a.energy_limit < a.center_limit;
+  const int items = OVF ? n_ovf : a.n_owned - a.slot_base;
+  const int chunks = (items + 31) / 32;
+  const int nwarps = gridDim.x * (kBlock / 32);
+
+  for (int chunk = blockIdx.x * (kBlock / 32) + tid / 32; chunk < chunks; chunk += nwarps) {
+    // ---- this lane's atom of the chunk, its count, the warp scan ----
+    const int q = chunk * 32 + lane;
+    const bool in = q < items;
+    int i = in ? (OVF ? a.ovf_in[q] : a.slot_base + q) : 0;
+    int n = in ? a.cnt[i] : 0;
+    if (!OVF && has_ghosts && in && (a.perm ? a.perm[i] : i) >= a.center_limit) {
+      // a decomposition ghost copy: receives forces, is not a centre
+      if (DET) {
+        Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+        f[0] = f[1] = f[2] = Acc(0);
+      }
+      n = 0;
+    }
+    if (n > 32) {                        // no wider launch behind this one
+      atomicOr(a.flags, kErrShortOverflow);
+      n = 0;
+    }
+    if (DET && in && n == 0) {           // no segment, no head: F_self = 0 here
+      Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+      f[0] = f[1] = f[2] = Acc(0);
+    }
+    int fgn = has_foreign && in && (a.perm ? a.perm[i] : i) >= a.energy_limit;
+#if TSF_PACKED_SORT
+    {
+      // order the chunk's atoms by count (bitonic, key (n, lane): unique, so
+      // deterministic): a pack then holds atoms of similar counts, and its
+      // rotations stop at a largest count that fits most of its lanes
+      int key = (n << 5) | lane;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          const int other = __shfl_xor_sync(kFull, key, jj);
+          const bool up = (lane & k) == 0, lower = (lane & jj) == 0;
+          key = (lower == up) ? min(key, other) : max(key, other);
+        }
+      const int src = key & 31;
+      i = __shfl_sync(kFull, i, src);
+      n = __shfl_sync(kFull, n, src);
+      fgn = __shfl_sync(kFull, fgn, src);
+    }
+#endif
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int excl = incl - n;
+    const int total = __shfl_sync(kFull, incl, 31);
+
+    for (int base = 0; base < total;) {           // warp-uniform: one pack per pass
+      const bool mine = n > 0 && excl >= base && incl <= base + 32;
+      const unsigned heads = __reduce_or_sync(kFull, mine ? 1u << (excl - base) : 0u);
+      const int used = int(__reduce_max_sync(kFull, mine ? unsigned(incl - base) : 0u));
+      if (mine) {
+        s_atom[wbase + excl - base] = i;
+        s_cnt[wbase + excl - base] = n;
+        s_fgn[wbase + excl - base] = fgn;
+      }
+      __syncwarp();
+      const bool slot = lane < used;
+      const int h = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // bit 0 is set
+      const int ai = s_atom[wbase + h];
+      const int ni = slot ? s_cnt[wbase + h] : 0;
+      const bool foreign = FOREIGN && s_fgn[wbase + h];
+      const int gl = lane - h;
+      const int v = slot ? a.nbr[ell_at(gl, ai, a.npad)] : ai;
+      const int j = unsigned(v) <= unsigned(last) ? v : ai;
+      const double4 pi = a.pos[ai];
+      const double4 pj = a.pos[j];
+
+      double dx = 0, dy = 0, dz = 0, r2 = 1.0;
+      if (slot) {
+        displacement(pi, pj, a.box, dx, dy, dz);
+        r2 = norm_sq_exact(dx, dy, dz);
+      }
+      const int si = SPEC == kSingle ? 0 : species_of(pi);
+      const int sj = SPEC == kSingle ? 0 : species_of(pj);
+      const int row_jj = (si * ns + sj) * ns + sj;
+      const bool pair_ok = slot && r2 <= (SPEC == kSingle ? cut0 : scut[row_jj]);
+      const Row<R>& pjj = SPEC == kSingle ? row0 : srow[row_jj];
+      Nbr<R> me;
+      me.ir = Fn<R>::rsqrt_(R(r2));
+      me.r = R(r2) * me.ir;
+      me.ux = R(dx) * me.ir;
+      me.uy = R(dy) * me.ir;
+      me.uz = R(dz) * me.ir;
+      R fc, dfc;
+      cutoff_ramp(me.r, pjj, fc, dfc);
+      const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
+      const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
+      const int meta = SPEC == kGeneric ? (slot ? sj : -1) : (pair_ok ? sj : -1);
+      st.put(tid, me, fc, dfc, meta);
+      if (SPEC == kGeneric) s_r2[tid] = r2;
+      __syncwarp();
+      const int rowbase = (si * ns + sj) * ns;
+      const int tmax = int(__reduce_max_sync(kFull, unsigned(ni)));
+
+      // partner of rotation t inside this lane's segment (itself once t >= n:
+      // its triplet is masked and its k-gradient is zero)
+      auto triplet_at = [&](int t) {
+        int m = gl;
+        if (t < ni) {
+          m = gl + t;
+          if (m >= ni) m -= ni;
+        }
+        const int src = wbase + h + m;
+        Nbr<R> k;
+        R fck, dfck, kmeta;
+        st.get(src, k, fck, dfck, kmeta);
+        bool ok = pair_ok && t < ni && kmeta >= R(0);
+        const Row<R>* prow = &pjj;
+        if (SPEC != kSingle) {
+          const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+          prow = &srow[rowbase + sk];
+          if (SPEC == kGeneric) {
+            ok = ok && s_r2[src] <= scut[rowbase + sk];
+            cutoff_ramp(k.r, *prow, fck, dfck);
+          }
+        }
+        fck = ok ? fck : R(0);
+        dfck = ok ? dfck : R(0);
+        return triplet<R>(me, k, fck, dfck, ok, *prow);
+      };
+
+      // ---- zeta pass ----
+      R zeta = 0, gjx = 0, gjy = 0, gjz = 0;
+      R ckx[kC + 1], cky[kC + 1], ckz[kC + 1];
+#pragma unroll
+      for (int t = 1; t <= kC; ++t) {
+        ckx[t] = cky[t] = ckz[t] = R(0);
+        if (t < tmax) {
+          const Grad<R> tr = triplet_at(t);
+          zeta += tr.z;
+          gjx += tr.jx;
+          gjy += tr.jy;
+          gjz += tr.jz;
+          ckx[t] = tr.kx;
+          cky[t] = tr.ky;
+          ckz[t] = tr.kz;
+        }
+      }
+      for (int t = kC + 1; t < tmax; ++t) {
+        const Grad<R> tr = triplet_at(t);
+        zeta += tr.z;
+        gjx += tr.jx;
+        gjy += tr.jy;
+        gjz += tr.jz;
+      }
+
+      // ---- pair block ----
+      R dvdr = 0, dvdz = 0, vv = 0;
+      if (pair_ok) {
+        const R dfr = -pjj.lam1 * fr;
+        const R dfa = -pjj.lam2 * fa;
+        R b, db;
+        bond_order(zeta, pjj, b, db);
+        const R rep = fr + b * fa;
+        vv = R(0.5) * fc * rep;
+        dvdr = R(0.5) * (dfc * rep + fc * (dfr + b * dfa));
+        dvdz = R(0.5) * fc * fa * db;
+        if (!isfinite(vv) || !isfinite(dvdr) || !isfinite(dvdz)) atomicOr(a.flags, kErrNonFinite);
+      }
+      R px = -(me.ux * dvdr) - gjx * dvdz;
+      R py = -(me.uy * dvdr) - gjy * dvdz;
+      R pz = -(me.uz * dvdr) - gjz * dvdz;
+
+      // ---- scatter: lane h + (gl - t) mod n sends its rotation-t k-gradient ----
+      auto receive = [&](int t, R sx, R sy, R sz) {
+        int s = gl;
+        if (t < ni) {
+          s = gl - t;
+          if (s < 0) s += ni;
+        }
+        const int from = h + s;
+        px -= __shfl_sync(kFull, sx, from);
+        py -= __shfl_sync(kFull, sy, from);
+        pz -= __shfl_sync(kFull, sz, from);
+      };
+#pragma unroll
+      for (int t = 1; t <= kC; ++t)
+        if (t < tmax) receive(t, ckx[t] * dvdz, cky[t] * dvdz, ckz[t] * dvdz);
+      for (int t = kC + 1; t < tmax; ++t) {
+        const Grad<R> tr = triplet_at(t);
+        receive(t, tr.kx * dvdz, tr.ky * dvdz, tr.kz * dvdz);
+      }
+      if (!slot) px = py = pz = 0;
+
+      // ---- F_i = -sum of the segment's P (and, queued + deterministic, the
+      // atom's energy and virial), summed by the head lane in slot order ----
+      const R rx = R(dx), ry = R(dy), rz = R(dz);
+      s_seg[0][tid] = Acc(px);
+      s_seg[1][tid] = Acc(py);
+      s_seg[2][tid] = Acc(pz);
+      if constexpr (OVF && DET) {
+        const bool cnt_ev = slot && !(FOREIGN && foreign);
+        s_seg[3][tid] = cnt_ev ? Acc(vv) : Acc(0);
+        s_seg[4][tid] = cnt_ev ? Acc(rx * px) : Acc(0);
+        s_seg[5][tid] = cnt_ev ? Acc(ry * py) : Acc(0);
+        s_seg[6][tid] = cnt_ev ? Acc(rz * pz) : Acc(0);
+        // the three off-diagonal components follow in a second round below
+      }
+      __syncwarp();
+      Acc fsum[3] = {0, 0, 0};
+      Acc evsum[7] = {0, 0, 0, 0, 0, 0, 0};
+      const bool head = slot && gl == 0;
+      if (head) {
+        for (int u = 0; u < ni; ++u) {
+          fsum[0] += s_seg[0][tid + u];
+          fsum[1] += s_seg[1][tid + u];
+          fsum[2] += s_seg[2][tid + u];
+          if constexpr (OVF && DET) {
+            evsum[0] += s_seg[3][tid + u];
+            evsum[1] += s_seg[4][tid + u];
+            evsum[2] += s_seg[5][tid + u];
+            evsum[3] += s_seg[6][tid + u];
+          }
+        }
+      }
+      if constexpr (OVF && DET) {
+        __syncwarp();
+        const bool cnt_ev = slot && !(FOREIGN && foreign);
+        s_seg[3][tid] = cnt_ev ? Acc(rx * py) : Acc(0);
+        s_seg[4][tid] = cnt_ev ? Acc(rx * pz) : Acc(0);
+        s_seg[5][tid] = cnt_ev ? Acc(ry * pz) : Acc(0);
+        __syncwarp();
+        if (head)
+          for (int u = 0; u < ni; ++u) {
+            evsum[4] += s_seg[3][tid + u];
+            evsum[5] += s_seg[4][tid + u];
+            evsum[6] += s_seg[5][tid + u];
+          }
+        if (head)
+#pragma unroll
+          for (int w = 0; w < 7; ++w) a.atom_ev[8 * std::size_t(ai) + w] = double(evsum[w]);
+      }
+      if (slot) {
+        if constexpr (!(OVF && DET)) if (!FOREIGN || !foreign) {
+          e_acc += Acc(vv);
+          w_acc[0] += Acc(rx * px);
+          w_acc[1] += Acc(ry * py);
+          w_acc[2] += Acc(rz * pz);
+          w_acc[3] += Acc(rx * py);
+          w_acc[4] += Acc(rx * pz);
+          w_acc[5] += Acc(ry * pz);
+        }
+        if (DET) {
+          const std::size_t qs = std::size_t(gl) * a.npad + ai;
+          static_cast<Acc*>(a.slot_x)[qs] = Acc(px);
+          static_cast<Acc*>(a.slot_y)[qs] = Acc(py);
+          static_cast<Acc*>(a.slot_z)[qs] = Acc(pz);
+        } else {
+          Acc* f = static_cast<Acc*>(a.forces) + 3 * std::size_t(j);
+          atomicAdd(f + 0, Acc(px));
+          atomicAdd(f + 1, Acc(py));
+          atomicAdd(f + 2, Acc(pz));
+        }
+      }
+      if (head) {
+        if (DET) {
+          Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(ai);
+          f[0] = -fsum[0];
+          f[1] = -fsum[1];
+          f[2] = -fsum[2];
+        } else {
+          Acc* f = static_cast<Acc*>(a.forces) + 3 * std::size_t(ai);
+          atomicAdd(f + 0, -fsum[0]);
+          atomicAdd(f + 1, -fsum[1]);
+          atomicAdd(f + 2, -fsum[2]);
+        }
+      }
+      base += used;
+      __syncwarp();                      // staging and heads are rewritten by the next pack
+    }
+  }
+
+  // ---- block reduction of energy + virial, fixed order ----
+  double red[7] = {double(e_acc), double(w_acc[0]), double(w_acc[1]), double(w_acc[2]),
+                   double(w_acc[3]), double(w_acc[4]), double(w_acc[5])};
+#pragma unroll
+  for (int qq = 0; qq < 7; ++qq)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) red[qq] += __shfl_down_sync(kFull, red[qq], o);
+  if (lane == 0)
+#pragma unroll
+    for (int qq = 0; qq < 7; ++qq) s_red[tid / 32][qq] = red[qq];
+  __syncthreads();
+  if (tid < kRedWidth) {
+    double s = 0;
+    if (tid < 7)
+      for (int w = 0; w < kBlock / 32; ++w) s += s_red[w][tid];
+    a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = s;
+  }
+}
+
+}  // namespace
+}  // namespace tsf

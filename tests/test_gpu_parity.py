@@ -449,3 +449,32 @@ def test_near_list_filter_is_exact(tb, kind, sic_text):
         assert abs(e1 - e2) <= 1e-13 * abs(e2) and np.abs(f1 - f2).max() <= 1e-12
     for c in (ctx, fresh):
         c.close()
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_packed_lane_groups(tb, oracle, sic_text, monkeypatch, mode):
+    """Packed lane groups (tsf_force_packed.cuh) against the oracle on the
+    irregular systems: TSF_PACKED=0 the G-tier chain, 1 (default) one packed
+    launch behind the G = 4 main launch (or packed from the start for
+    irregular systems), 2 packed main launch everywhere — all precisions,
+    both scatter modes; deterministic mode bitwise reproducible."""
+    monkeypatch.setenv("TSF_PACKED", mode)
+    for case in [systems.dense_random(tb), systems.liquid_like(tb, 4, 0.35, 5),
+                 systems.zincblende(tb, sic_text, 4, jitter=0.1, seed=1, skin=0.5),
+                 systems.perturbed(tb, 4, 0.12, 32, skin=0.5)]:
+        params, ctx = _ctx(tb, case)
+        _, _, _, ref = _oracle(oracle, case, params)
+        fscale = max(1.0, np.abs(ref["forces"]).max())
+        for det in (True, False):
+            e, f, w = ctx.compute("double", deterministic=det)
+            assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"]), (case.name, det)
+            assert np.abs(f - ref["forces"]).max() <= F_TOL_D * fscale, (case.name, det)
+            assert np.abs(w - ref["virial"]).max() <= 1e-10 * max(1.0, np.abs(ref["virial"]).max())
+            for prec in ("mixed", "single"):
+                e, f, _ = ctx.compute(prec, deterministic=det)
+                assert abs(e - ref["energy"]) <= E_TOL_M * abs(ref["energy"]), (case.name, prec)
+                assert np.abs(f - ref["forces"]).max() <= F_TOL_M * fscale, (case.name, prec)
+        e1, f1, w1 = ctx.compute("double", deterministic=True)
+        e2, f2, w2 = ctx.compute("double", deterministic=True)
+        assert e1 == e2 and np.array_equal(f1, f2) and np.array_equal(w1, w2)
+        ctx.close()
