@@ -275,12 +275,27 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / timed,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": DTYPES[args.precision], "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][4], "n_atoms": n,
-                   "precision": args.precision},
+        "config": workload_config(args, n, world, None, None),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def workload_config(args, n, world, halo, parallelism):
+    """The `config` object of both arms' lines: the workload, not the
+    implementation (the driver compares the two arms' configs)."""
+    jit = CONFIGS[args.config][2]
+    return {
+        "workload": CONFIGS[args.config][4] + (f", seeded uniform +-{jit:.2f} A jitter" if jit
+                                               else "") +
+                    ", skin 1.0 A; one filter + force/energy/virial evaluation per step",
+        "n_atoms": n, "precision": args.precision,
+        "deterministic": bool(args.deterministic),
+        "parallelism": parallelism or (f"{world} x-slab domains" if world > 1 else "single GPU"),
+        "l2": "inputs larger than L2 (positions + lists + forces > 126 MB at 2M atoms)"
+              if n >= 1_000_000 else "inputs fit in L2",
+    }
 
 
 def cpu_baseline(text, xyz, species, box, per, masses):
@@ -411,6 +426,15 @@ def main():
         def step():
             dec.evaluate(args.precision, args.deterministic)
     algo_flop = 75 * P + 143 * T
+    if use_dec:
+        parallelism = (f"{world} x-slab domains, ghost halo {halo:.1f} A, "
+                       + ("ghost-centre mode: one forward exchange of positions per step, no "
+                          "reverse force exchange" if dec.ghost_centers else
+                          "forward positions and reverse ghost forces each step")
+                       + (", exchange overlapped with the interior centres" if dec.overlap
+                          else "") + " (NCCL P2P)")
+    else:
+        parallelism = "single GPU"
 
     clocks = ClockSampler(local)       # running before the warm-up
     # NVTX range around the steady state: ncu captures (tools/ncu_*.sh) use
@@ -591,18 +615,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": DTYPES[args.precision], "data": "synthetic",
-            "config": {
-                "workload": CONFIGS[args.config][4] + ", seeded uniform +-%.2f A jitter, skin "
-                            "1.0 A; one filter + force/energy/virial evaluation per step"
-                            % CONFIGS[args.config][2],
-                "n_atoms": n, "precision": args.precision,
-                "scatter": "deterministic gather" if args.deterministic else "atomics",
-                "parallelism": (f"{world} x-slab domains, ghost halo {params.r_cut_max + skin:.1f} A,"
-                                " NCCL P2P forward positions / reverse forces each step"
-                                if world > 1 else "single GPU"),
-                "l2": "inputs larger than L2 (positions + lists + forces > 126 MB at 2M atoms)"
-                      if n >= 1_000_000 else "inputs fit in L2",
-            },
+            "config": workload_config(args, n, world, params.r_cut_max + skin, parallelism),
             "roofline": {
                 "bound": "fp64" if args.precision == "double" else "fp32",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

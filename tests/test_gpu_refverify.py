@@ -78,3 +78,21 @@ def test_reference_acceptance_gate(criterion):
         pytest.skip("oracle/_ref/acceptance_b200 not built (needs /root/reference at build time)")
     p = subprocess.run([ACC, str(criterion)], capture_output=True, text=True, timeout=900)
     assert p.returncode == 0 and p.stdout.startswith("PASS"), p.stdout + p.stderr
+
+
+def test_engine_run_through_the_drop_in():
+    """tmd::Engine::run (engine.cpp:174-199) on cfg 2 with the B200 drop-in as
+    evaluate_forces follows the stock CPU Engine: same rebuild schedule, Etot
+    within 1e-9 relative after 100 steps (oracle/engine_run_main.cpp)."""
+    import json
+    b200 = os.path.join(ROOT, "oracle", "_ref", "engine_run_b200")
+    cpu = os.path.join(ROOT, "oracle", "_ref", "engine_run_cpu")
+    if not (os.path.exists(b200) and os.path.exists(cpu)):
+        pytest.skip("oracle/_ref/engine_run_* not built (needs /root/reference at build time)")
+    rg = json.loads(subprocess.run([b200, "100"], capture_output=True, text=True,
+                                   timeout=600).stdout)
+    rc = json.loads(subprocess.run([cpu, "100"], capture_output=True, text=True,
+                                   timeout=600).stdout)
+    assert rg["rebuilds"] == rc["rebuilds"] == 4
+    assert abs(rg["etot_first"] - rc["etot_first"]) <= 1e-12 * abs(rc["etot_first"])
+    assert abs(rg["etot_last"] - rc["etot_last"]) <= 1e-9 * abs(rc["etot_last"])
