@@ -353,6 +353,65 @@ def md_leg(tb, params, args):
             "rel_energy_drift": float(np.abs(etot - etot[0]).max() / abs(etot[0]))}
 
 
+def md_leg_dd(tb, params, args, world, rank, local):
+    """The MD leg across x slabs: tsf_dd_md_run (velocity Verlet, the
+    needs_rebuild OR over ranks on the device, atom migration and ghost
+    re-selection at rebuilds) on the workload's lattice at 1600 K; CUDA events
+    on each rank's stream, max over ranks."""
+    import torch
+    from paper_1607_02904_b200 import parallel as PD
+    cells = CONFIGS[args.config][0]
+    s = tb.make_diamond_lattice(*cells, CONFIGS[args.config][1])
+    tb.init_velocities(s, 1600.0, 12345)
+    box = s.box.lengths
+    halo = params.r_cut_max + 1.0
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(PD.nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, 0)
+        transport, unique_id = "nccl", bytes(uid.cpu().numpy())
+    else:
+        transport, unique_id = PD.LocalGroup(1), None
+    dd = PD.DomainDecomposition(params, local, box, s.box.periodic, params.r_cut_max, 1.0,
+                                transport, rank, world=world, unique_id=unique_id,
+                                masses=s.species_masses,
+                                ghost_centers=box[0] / world > 4 * halo + 1e-9)
+    gid = PD.partition(s.positions, box, world, rank)
+    dd.setup(gid, s.positions[gid], s.species[gid], s.velocities[gid])
+    det = args.deterministic
+    dd.md_run(max(args.warmup, 20), 0.001, args.precision, det, 100)
+    steps = max(100, args.steps)
+    stream = torch.cuda.ExternalStream(dd.stream, device=local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    thermo, rebuilds = dd.md_run(steps, 0.001, args.precision, det, 100)
+    e1.record(stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    migrated = dd.counts["migrated"]
+    dd.close()
+    etot = thermo[:, 1] + thermo[:, 2]
+    n = s.natoms
+    return {"metric": "MD atom-steps/s", "value": n * steps / t, "unit": UNIT,
+            "ms_per_step": 1e3 * t / steps, "steps": steps, "rebuilds": int(rebuilds),
+            "atoms_migrated_rank0": int(migrated),
+            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": args.precision,
+            "scatter": "deterministic gather" if det else "atomics",
+            "workload": f"{CONFIGS[args.config][4]}, perfect lattice + init_velocities(1600 K, "
+                        f"seed 12345), dt 1 fs, skin 1 A, {world} x slabs (tsf_dd_md_run: "
+                        "ghost exchange every step, migration at rebuilds)",
+            "rel_energy_drift": float(np.abs(etot - etot[0]).max() / abs(etot[0]))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -404,35 +463,46 @@ def main():
             ctx.compute(args.precision, deterministic=args.deterministic, energy=False,
                         forces=False, virial=False)
     else:
-        # strong scaling: the same global system split into x slabs, ghost
-        # positions forward and ghost forces back every step (NCCL P2P)
-        from paper_1607_02904_b200.parallel import Decomposition, GpuEngine, partition
+        # strong scaling: the same global system split into x slabs, one rank
+        # per GPU, the C++ decomposition (csrc/tsf_dd.cu) over NCCL: ghost
+        # positions forward (and, in classic mode, ghost forces back) every step
+        from paper_1607_02904_b200 import parallel as PD
         halo = params.r_cut_max + skin
-        eng = GpuEngine(params, local)
-        # ghost-centre mode (one exchange per step, no reverse force exchange)
-        # when the slabs are wide enough for its 2-halo ghost shell
-        # and the forward exchange overlapped with the interior centres' compute
-        dec = Decomposition(eng, box, per, halo, ghost_centers=box[0] / world >= 4 * halo,
-                            overlap=True)
-        gid = partition(xyz, box, world, rank, halo)
-        dec.setup(gid, xyz[gid], species[gid], params.r_cut_max, skin)
-        ctx = eng.ctx
-        stream = torch.cuda.current_stream(local)
-        soff, snb = ctx.export_neighbors("short")     # this rank's launch: owned centres
-        no = dec.n_owned
-        P, T = algorithmic_work(dec.local_xyz, dec.local_species, box, soff[: no + 1],
-                                snb[: soff[no]], params.rows, params.species_count)
+        ghost_centers = box[0] / world > 4 * halo + 1e-9
+        if world > 1:
+            uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(PD.nccl_unique_id()), dtype=torch.uint8))
+            torch.distributed.broadcast(uid, 0)
+            transport, unique_id = "nccl", bytes(uid.cpu().numpy())
+        else:       # --decompose: the same code path, one in-process rank
+            transport, unique_id = PD.LocalGroup(1), None
+        dec = PD.DomainDecomposition(params, local, box, per, params.r_cut_max, skin, transport,
+                                     rank, world=world, unique_id=unique_id,
+                                     ghost_centers=ghost_centers)
+        gid = PD.partition(xyz, box, world, rank)
+        dec.setup(gid, xyz[gid], species[gid])
+        ctx = dec.ctx
+        stream = torch.cuda.ExternalStream(dec.stream, device=local)
+        # the whole job's algorithmic work (every centre once): the global short
+        # list of a throw-away single context on this rank's GPU
+        tmp = tb.Context(params, local)
+        tmp.set_system(xyz, species, box, per)
+        tmp.build_neighbor_list(params.r_cut_max, skin)
+        soff, snb = tmp.export_neighbors("short")
+        tmp.close()
+        P, T = algorithmic_work(xyz, species, box, soff, snb, params.rows, params.species_count)
+        del soff, snb
 
         def step():
             dec.evaluate(args.precision, args.deterministic)
     algo_flop = 75 * P + 143 * T
     if use_dec:
-        parallelism = (f"{world} x-slab domains, ghost halo {halo:.1f} A, "
+        parallelism = (f"{world} x-slab domains (C++ tsf_dd), ghost halo {halo:.1f} A, "
                        + ("ghost-centre mode: one forward exchange of positions per step, no "
-                          "reverse force exchange" if dec.ghost_centers else
+                          "reverse force exchange" if ghost_centers else
                           "forward positions and reverse ghost forces each step")
-                       + (", exchange overlapped with the interior centres" if dec.overlap
-                          else "") + " (NCCL P2P)")
+                       + (" (NCCL P2P)" if world > 1 else " (one in-process rank)"))
     else:
         parallelism = "single GPU"
 
@@ -487,7 +557,8 @@ def main():
     stage_s = (prof["force_ms"] + prof["tail_ms"]) / calls / 1e3
     stage_total = prof["filter_ms"] + prof["setup_ms"] + prof["force_ms"] + prof["tail_ms"]
     peak, peak_src = load_peak(args.precision)
-    achieved = algo_flop / stage_s / 1e12
+    # per GPU: the whole job's work over the ranks (x slabs of equal width)
+    achieved = algo_flop / world / stage_s / 1e12
     ncu_traffic, ncu_issue = load_ncu(args.config, args.precision, args.deterministic)
 
     # e2e through the drop-in C-ABI call with host buffers
@@ -495,17 +566,14 @@ def main():
     if not args.no_e2e and use_dec:
         # per rank: owned positions in from pinned host memory, decomposed
         # evaluation (ghost exchange both ways), owned forces back to the host
-        hx = torch.from_numpy(xyz[dec.gid].copy()).pin_memory()
-        dx = torch.empty(hx.shape, dtype=torch.float64, device=f"cuda:{local}")
-        hf = torch.empty((dec.n_owned, 3), dtype=torch.float64).pin_memory()
+        own = dec.results()
+        hx = torch.from_numpy(xyz[own["gid"]].copy()).pin_memory()
+        hf = torch.empty((len(own["gid"]), 3), dtype=torch.float64).pin_memory()
 
         def call():
-            dx.copy_(hx, non_blocking=True)
-            eng.scatter_positions(0, dx)
+            dec.set_positions_ptr(hx.data_ptr())
             dec.evaluate(args.precision, args.deterministic)
-            _, fu = eng.results()
-            hf.copy_(fu[: dec.n_owned], non_blocking=True)
-            stream.synchronize()
+            dec.forces_into(hf.data_ptr())
         for _ in range(args.warmup):
             call()
         barrier()
@@ -523,8 +591,9 @@ def main():
         e2e = {"value": n * args.steps / te, "unit": UNIT,
                "h2d_bytes_per_step": int(24 * n), "d2h_bytes_per_step": int(24 * n),
                "ms_per_step": 1e3 * te / args.steps,
-               "call": "per rank: owned positions H2D (pinned), Decomposition.evaluate, "
-                       "owned forces D2H; bytes summed over ranks"}
+               "call": "per rank: owned positions H2D (tsf_dd_set_positions, pinned), "
+                       "tsf_dd_evaluate, owned forces D2H (tsf_dd_results); bytes summed over "
+                       "ranks"}
     elif not args.no_e2e:
         lib = L.lib()
         hx = torch.from_numpy(xyz.copy()).pin_memory()
@@ -602,8 +671,9 @@ def main():
     # kick, drift, the needs_rebuild test every step, list rebuilds, the
     # evaluation — timed with CUDA events on the context's stream
     md = None
-    if world == 1 and not args.no_md and args.config in ("si2m", "si32k"):
-        md = md_leg(tb, params, args)
+    if not args.no_md and args.config in ("si2m", "si32k"):
+        md = md_leg_dd(tb, params, args, world, rank, local) if use_dec else \
+            md_leg(tb, params, args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

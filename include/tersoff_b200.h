@@ -199,6 +199,55 @@ int tsf_add_forces(tsf_ctx* ctx, const int32_t* d_idx, int64_t m, const double* 
 /* device copies of the latest results: d_out[0] energy, [1..6] virial; forces[n][3] user order */
 int tsf_results_device(tsf_ctx* ctx, double* d_energy_virial, double* d_forces);
 
+/* ---- spatial domain decomposition in C++  ----------------
+ * One rank per GPU, x slabs of equal width (periodic x, slabs wider than two
+ * ghost reaches), global frame and global box.  Each rank's context holds
+ * [owned (sorted by global id) | ghosts]; ghost selection, the per-step ghost
+ * position exchange, the reverse ghost-force exchange, atom migration at
+ * rebuilds and the velocity-Verlet loop run on the device; the host only
+ * sizes buffers at rebuilds.  Transports: NCCL (libnccl.so.2 loaded at run
+ * time; rank 0 makes the unique id, the caller distributes it) or LOCAL —
+ * several ranks of one process, each driven by its own host thread, sharing
+ * a group (tests and per-rank projections on one GPU).
+ * TSF_DD_GHOST_CENTERS: ghosts within two halos, the first layer also acts as
+ * centres — one exchange per step, no reverse force exchange.
+ * Errors: the return codes above; messages via tsf_dd_error_message(). */
+typedef struct tsf_dd tsf_dd;
+typedef struct tsf_dd_group tsf_dd_group;
+#define TSF_DD_GHOST_CENTERS 0x1u
+const char* tsf_dd_error_message(void);
+int tsf_dd_nccl_unique_id(uint8_t* id /* 128 bytes */);
+int tsf_dd_create_nccl(tsf_ctx* ctx, int world, int rank, const uint8_t* id, double cutoff,
+                       double skin, const double box[3], const uint8_t periodic[3],
+                       const double* masses /* S, may be NULL */, uint32_t mode, tsf_dd** out);
+int tsf_dd_group_create(int world, tsf_dd_group** out);
+void tsf_dd_group_destroy(tsf_dd_group* group);
+int tsf_dd_create_local(tsf_ctx* ctx, tsf_dd_group* group, int rank, double cutoff, double skin,
+                        const double box[3], const uint8_t periodic[3], const double* masses,
+                        uint32_t mode, tsf_dd** out);
+void tsf_dd_destroy(tsf_dd* dd);
+/* this rank's owned atoms (host arrays, any order); vel may be NULL */
+int tsf_dd_setup(tsf_dd* dd, int64_t n_owned, const int64_t* gid, const double* xyz,
+                 const int32_t* species, const double* vel);
+/* forward ghost exchange, evaluation, reverse exchange, energy/virial allreduce */
+int tsf_dd_evaluate(tsf_dd* dd, int precision, uint32_t flags);
+/* migration + ghost re-selection + list build now (collective) */
+int tsf_dd_rebuild(tsf_dd* dd);
+/* distributed NVE: as tsf_md_run; thermo samples are global (summed over ranks) */
+int tsf_dd_md_run(tsf_dd* dd, int precision, int64_t steps, double dt, uint32_t flags,
+                  int thermo_every, double* thermo, int64_t cap, int64_t* nsamples,
+                  int64_t* rebuilds);
+/* new positions of this rank's owned atoms (host, gid order as returned by
+ * tsf_dd_results); ghosts follow at the next evaluation's exchange */
+int tsf_dd_set_positions(tsf_dd* dd, const double* xyz);
+/* counts[8]: owned, centres, local atoms, sent left, sent right, rebuilds,
+ * atoms received by migration, ghost-centre mode */
+int tsf_dd_counts(tsf_dd* dd, int64_t* counts);
+/* global energy + virial (7), and this rank's owned atoms in gid order:
+ * gid[n_owned], positions, forces, velocities (any pointer may be NULL) */
+int tsf_dd_results(tsf_dd* dd, double* energy_virial, int64_t* gid, double* xyz, double* forces,
+                   double* vel);
+
 /* ---- GPU-resident velocity-Verlet NVE (engine.cpp:142-199) ------------- */
 int tsf_md_set_state(tsf_ctx* ctx, const double* vel, const double* masses /* S */);
 int tsf_md_get_state(tsf_ctx* ctx, double* xyz, double* vel);

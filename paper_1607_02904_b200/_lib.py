@@ -96,6 +96,23 @@ PROTOTYPES = [
     ("tsf_gather_forces", C.c_int, [_vp, C.c_int64, C.c_int64, _vp]),
     ("tsf_add_forces", C.c_int, [_vp, _vp, C.c_int64, _vp]),
     ("tsf_results_device", C.c_int, [_vp, _vp, _vp]),
+    ("tsf_dd_error_message", C.c_char_p, []),
+    ("tsf_dd_nccl_unique_id", C.c_int, [_vp]),
+    ("tsf_dd_create_nccl", C.c_int, [_vp, C.c_int, C.c_int, _vp, _d, _d, _vp, _vp, _vp,
+                                     C.c_uint32, _pp]),
+    ("tsf_dd_group_create", C.c_int, [C.c_int, _pp]),
+    ("tsf_dd_group_destroy", None, [_vp]),
+    ("tsf_dd_create_local", C.c_int, [_vp, _vp, C.c_int, _d, _d, _vp, _vp, _vp, C.c_uint32,
+                                      _pp]),
+    ("tsf_dd_destroy", None, [_vp]),
+    ("tsf_dd_setup", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp]),
+    ("tsf_dd_evaluate", C.c_int, [_vp, C.c_int, C.c_uint32]),
+    ("tsf_dd_rebuild", C.c_int, [_vp]),
+    ("tsf_dd_md_run", C.c_int, [_vp, C.c_int, C.c_int64, _d, C.c_uint32, C.c_int, _vp,
+                                C.c_int64, _i64p, _i64p]),
+    ("tsf_dd_set_positions", C.c_int, [_vp, _vp]),
+    ("tsf_dd_counts", C.c_int, [_vp, _vp]),
+    ("tsf_dd_results", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("tsf_md_scale_velocities", C.c_int, [_vp, C.c_double]),
     ("tsf_md_kick", C.c_int, [_vp, _d, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     ("tsf_md_kinetic", C.c_int, [_vp, _dptr]),

@@ -69,6 +69,7 @@ template struct DevBuf<unsigned long long>;
 template struct DevBuf<unsigned>;
 template struct DevBuf<Row<double>>;
 template struct DevBuf<Row<float>>;
+template struct DevBuf<long long>;
 
 void ensure_pinned(Ctx& c, std::size_t doubles) {
   if (doubles <= c.pinned_cap) return;
@@ -151,15 +152,8 @@ void upload_xyz(Ctx& c, const double* xyz) {
   c.forces_current = false;
 }
 
-void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* species,
-                const double* box, const std::uint8_t* per) {
-  if (n < 0 || n > (std::int64_t(1) << 30)) throw tsf::ConfigError("atom count out of range");
-  for (int ax = 0; ax < 3; ++ax)
-    if (!(box[ax] > 0.0)) throw tsf::ConfigError("simulation box edges must be positive");
-  // page-locked species go straight to the device and are validated there (no
-  // O(n) host pass per call); pageable ones are checked and cached on the host
-  const bool sp_pinned = n > 0 && is_pinned(species);
-  if (!sp_pinned) check_species(c, n, species);
+// Atom count and box of a set_system call: reallocation, list invalidation.
+void set_geometry(Ctx& c, std::int64_t n, const double* box, const std::uint8_t* per) {
   bool geometry_changed = n != c.n;
   for (int ax = 0; ax < 3; ++ax) {
     geometry_changed |= c.box.len[ax] != box[ax] || c.box.per[ax] != int(per[ax] != 0);
@@ -194,6 +188,18 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
     c.short_list.valid = false;
     c.tiled = false;
   }
+}
+
+void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* species,
+                const double* box, const std::uint8_t* per) {
+  if (n < 0 || n > (std::int64_t(1) << 30)) throw tsf::ConfigError("atom count out of range");
+  for (int ax = 0; ax < 3; ++ax)
+    if (!(box[ax] > 0.0)) throw tsf::ConfigError("simulation box edges must be positive");
+  // page-locked species go straight to the device and are validated there (no
+  // O(n) host pass per call); pageable ones are checked and cached on the host
+  const bool sp_pinned = n > 0 && is_pinned(species);
+  if (!sp_pinned) check_species(c, n, species);
+  set_geometry(c, n, box, per);
   if (sp_pinned) {
     TSF_CUDA(cudaMemcpyAsync(c.species.get(), species, sizeof(int) * n, cudaMemcpyHostToDevice,
                              c.stream));
@@ -405,6 +411,60 @@ void evaluate(Ctx& c, tsf::Precision p, std::uint32_t flags) {
     ++c.profiled_calls;
   }
 }
+
+}  // namespace
+
+// Context operations for the other translation units (tsf_dd.cu: the domain
+// decomposition drives a context with device-resident inputs).
+namespace tsf {
+void evaluate_ctx(Ctx& c, Precision p, std::uint32_t flags) { evaluate(c, p, flags); }
+void raise_errors(Ctx& c) { raise_device_errors(c); }
+// set_system with device arrays (positions AoS [n][3] user order, species)
+void set_system_device(Ctx& c, std::int64_t n, const double* d_xyz, const int* d_species,
+                       const double* box, const std::uint8_t* per) {
+  if (n < 0 || n > (std::int64_t(1) << 30)) throw ConfigError("atom count out of range");
+  for (int ax = 0; ax < 3; ++ax)
+    if (!(box[ax] > 0.0)) throw ConfigError("simulation box edges must be positive");
+  set_geometry(c, n, box, per);
+  c.host_species.clear();
+  if (n == 0) return;
+  TSF_CUDA(cudaMemcpyAsync(c.species.get(), d_species, sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                           c.stream));
+  validate_species(c, c.has_potential ? c.params.species_count() : kMaxListSpecies);
+  TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), d_xyz, 3 * n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + 5, 0, sizeof(int), c.stream));
+  pack_positions(c);
+  c.forces_current = false;
+}
+// velocities (AoS [n][3] user order) from device memory; masses per species
+void set_velocities_device(Ctx& c, const double* d_vel, const double* masses) {
+  const int s = c.params.species_count();
+  for (int q = 0; q < s; ++q)
+    if (!(masses[q] > 0.0)) throw ConfigError("species " + std::to_string(q) + " has non-positive mass");
+  c.masses.assign(masses, masses + s);
+  if (c.n == 0) return;
+  TSF_CUDA(cudaMemcpyAsync(c.xyz_stage.get(), d_vel, 3 * c.n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c.stream));
+  pack_velocities(c);
+}
+// user-order positions / velocities of atoms [0, m) into device arrays
+void get_state_device(Ctx& c, std::int64_t m, double* d_xyz, double* d_vel) {
+  if (m <= 0) return;
+  if (d_xyz) {
+    unpack_positions(c);
+    TSF_CUDA(cudaMemcpyAsync(d_xyz, c.xyz_stage.get(), 3 * m * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c.stream));
+  }
+  if (d_vel) {
+    unpack_velocities(c);
+    TSF_CUDA(cudaMemcpyAsync(d_vel, c.xyz_stage.get(), 3 * m * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c.stream));
+  }
+}
+}  // namespace tsf
+
+namespace {
 
 int compute_entry(tsf_ctx* ctx, tsf::Precision p, std::uint32_t flags, double* e, double* f,
                   double* w) {

@@ -341,9 +341,19 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       active = a.slot_base + work * kAtomsPerBlock + tid / G < a.n_owned;
       // ghost copies (decomposition) receive forces but are not centers
       if (active && ghost) {
-        if (DET && gl == 0) {
-          Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
-          f[0] = f[1] = f[2] = Acc(0);
+        if (DET) {
+          // a ghost contributes nothing here (its owner evaluates it): zero
+          // its self term and the slots k_gather reads for its neighbours
+          if (gl == 0) {
+            Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+            f[0] = f[1] = f[2] = Acc(0);
+          }
+          for (int sl = gl; sl < n_i; sl += G) {
+            const std::size_t q = std::size_t(sl) * a.npad + i;
+            static_cast<Acc*>(a.slot_x)[q] = Acc(0);
+            static_cast<Acc*>(a.slot_y)[q] = Acc(0);
+            static_cast<Acc*>(a.slot_z)[q] = Acc(0);
+          }
         }
         active = false;
       }

@@ -97,9 +97,15 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
     int n = in ? a.cnt[i] : 0;
     if (!OVF && has_ghosts && in && (a.perm ? a.perm[i] : i) >= a.center_limit) {
       // a decomposition ghost copy: receives forces, is not a centre
-      if (DET) {
+      if (DET) {   // zero its self term and the slots k_gather reads
         Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
         f[0] = f[1] = f[2] = Acc(0);
+        for (int sl = 0; sl < n; ++sl) {
+          const std::size_t qs = std::size_t(sl) * a.npad + i;
+          static_cast<Acc*>(a.slot_x)[qs] = Acc(0);
+          static_cast<Acc*>(a.slot_y)[qs] = Acc(0);
+          static_cast<Acc*>(a.slot_z)[qs] = Acc(0);
+        }
       }
       n = 0;
     }

@@ -123,7 +123,7 @@ class _Mailbox:
 
 def _emulated(tb, mail, rank, world, c, out, ghost_centers=False, overlap=False, det=True):
     """One emulated rank: Decomposition with a mailbox exchange (host copies)."""
-    from paper_1607_02904_b200 import parallel as P
+    import dd_model as P
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -200,7 +200,7 @@ def test_slab_nve_single_rank_matches_md_run(tb):
     Decomposition.migrate/setup) reproduces the fused GPU-resident loop
     tsf_md_run step for step in deterministic mode: same rebuild schedule,
     same thermo samples, same final state."""
-    from paper_1607_02904_b200.parallel import Decomposition, GpuEngine, SlabNVE
+    from dd_model import Decomposition, GpuEngine, SlabNVE
     params = tb.builtin_silicon()
     s = tb.make_diamond_lattice(4, 4, 4)
     tb.init_velocities(s, 1600.0, 12345)

@@ -128,7 +128,7 @@ def _worker(rank, world, port, cells, shift, out_path, ghost_centers=False, over
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.oracle import Oracle
-        from paper_1607_02904_b200.parallel import Decomposition, partition
+        from dd_model import Decomposition, partition
         c = _case(cells)
         halo = 3.2 + c.skin
         gid = partition(c.xyz, c.box, world, rank, halo)
@@ -191,7 +191,7 @@ def test_reverse_exchange_split_add(oracle, tmp_path):
 
 
 def test_slab_geometry_guards():
-    from paper_1607_02904_b200.parallel import Slab
+    from dd_model import Slab
     s = Slab(rank=1, world=4, length=40.0, halo=3.0)
     assert (s.lo, s.hi) == (10.0, 20.0)
     x = np.array([10.0, 12.9, 13.1, 17.0, 19.99, 39.9])
@@ -207,7 +207,7 @@ def _nve_worker(rank, world, port, steps, out_path, nx=5, ghost_centers=False, o
     try:
         import paper_1607_02904_b200 as tb
         from oracle.oracle import Oracle
-        from paper_1607_02904_b200.parallel import Decomposition, SlabNVE, partition
+        from dd_model import Decomposition, SlabNVE, partition
         c = _nve_case(nx)
         s = tb.make_diamond_lattice(nx, 2, 2)
         tb.init_velocities(s, 3000.0, 7)

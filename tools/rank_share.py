@@ -30,10 +30,11 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import bench  # noqa: E402  (make_system: the bench's own synthetic input)
 import paper_1607_02904_b200 as tb  # noqa: E402
-from paper_1607_02904_b200 import parallel as P  # noqa: E402
+import dd_model as P  # noqa: E402
 
 
 class Mailbox:
