@@ -10,6 +10,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bounds checks of a checked build (make EXTRA=-DTSF_BOUNDS_CHECK;
+// tools/checked_build.sh): every list entry, slot and gather index the hot
+// kernels use is asserted in range, and a violation traps with its location.
+// compute-sanitizer is not available on this pool, so this build plus the
+// small-case sweep (tools/sanitize_case.py) stands in for memcheck.
+#ifdef TSF_BOUNDS_CHECK
+#include <cstdio>
+#define TSF_DCHECK(cond, what)                                                       \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("tsf bounds check failed: %s (%s:%d)\n", what, __FILE__, __LINE__);     \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define TSF_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace tsf {
 
 constexpr int kMaxSpecies = 4;          // S^3 <= 64 parameter rows

@@ -289,8 +289,10 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     t.i = a.slot_base + tile * kAtomsPerBlock + tid / G;
     const bool in = tile < ntiles && t.i < a.n_owned;
     if (!in) t.i = 0;
+    TSF_DCHECK(!in || (t.i >= 0 && t.i < a.n_all), "k_force centre slot");
     t.n = in ? a.cnt[t.i] : 0;
     const int v = in ? a.nbr[ell_at(gl, t.i, a.npad)] : 0;
+    TSF_DCHECK(!in || gl >= t.n || (v >= 0 && v <= last && v != t.i), "k_force list entry");
     t.j = unsigned(v) <= unsigned(last) ? v : 0;
     // ghost tests two tiles ahead (the perm[] load at the tile start was 24%
     // of the stall samples, ncu); skipped when the context has no ghosts
@@ -576,6 +578,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         w_acc[4] += Acc(rx * pz);
         w_acc[5] += Acc(ry * pz);
       }
+      TSF_DCHECK(j >= 0 && j <= last && i >= 0 && i <= last, "k_force scatter target");
       if (DET) {
         const std::size_t q = std::size_t(gl) * a.npad + i;
         static_cast<Acc*>(a.slot_x)[q] = Acc(px);
@@ -703,6 +706,7 @@ __global__ void __launch_bounds__(kBlock) k_gather(int n, int npad, const int* _
   const int m = cnt[a];
   for (int s = 0; s < m; ++s) {
     const int b = nbr[ell_at(s, a, npad)];
+    TSF_DCHECK(b >= 0 && b < n && b != a, "k_gather list entry");
     const int mb = cnt[b];
     for (int t = 0; t < mb; ++t) {
       if (nbr[ell_at(t, b, npad)] == a) {

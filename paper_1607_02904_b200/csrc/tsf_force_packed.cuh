@@ -163,7 +163,10 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       const int ni = slot ? s_cnt[wbase + h] : 0;
       const bool foreign = FOREIGN && s_fgn[wbase + h];
       const int gl = lane - h;
+      TSF_DCHECK(h >= 0 && h <= lane && ai >= 0 && ai <= last, "k_force_packed segment head");
+      TSF_DCHECK(!slot || (gl < ni && ni <= 32), "k_force_packed segment slot");
       const int v = slot ? a.nbr[ell_at(gl, ai, a.npad)] : ai;
+      TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
       const int j = unsigned(v) <= unsigned(last) ? v : ai;
       const double4 pi = a.pos[ai];
       const double4 pj = a.pos[j];
@@ -303,6 +306,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       Acc fsum[3] = {0, 0, 0};
       Acc evsum[7] = {0, 0, 0, 0, 0, 0, 0};
       const bool head = slot && gl == 0;
+      TSF_DCHECK(!head || lane + ni <= 32, "k_force_packed segment sum");
       if (head) {
         for (int u = 0; u < ni; ++u) {
           fsum[0] += s_seg[0][tid + u];

@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(kBlock) k_skin_list(ListArgs a, double bc, dou
         const int row = (pick(sz, iz) * g.nc[1] + pick(sy, iy)) * g.nc[0] + cls * ncells;
         for (int ix = 0; ix < mx; ++ix) {
           const int c = row + pick(sx, ix);
+          TSF_DCHECK(c >= 0 && c < ncells * a.ncls, "k_skin_list stencil cell");
           const int b1 = a.start[c + 1];
+          TSF_DCHECK(a.start[c] >= 0 && b1 <= a.n && a.start[c] <= b1, "k_skin_list cell range");
           for (int b = a.start[c]; b < b1; ++b) {
             if (b == at) continue;
             const float r2 = dist2f(pfa, a.posf[b], wrap);
@@ -314,6 +316,10 @@ __device__ __forceinline__ void test_block(const ListArgs& a, const FilterBands&
   e.y &= 0x7fffffff;
   e.z &= 0x7fffffff;
   e.w &= 0x7fffffff;
+  TSF_DCHECK(valid <= 0 || (e.x >= 0 && e.x < a.n && e.x != at), "k_filter entry 0");
+  TSF_DCHECK(valid <= 1 || (e.y >= 0 && e.y < a.n && e.y != at), "k_filter entry 1");
+  TSF_DCHECK(valid <= 2 || (e.z >= 0 && e.z < a.n && e.z != at), "k_filter entry 2");
+  TSF_DCHECK(valid <= 3 || (e.w >= 0 && e.w < a.n && e.w != at), "k_filter entry 3");
   const int bb[4] = {valid > 0 && !(sure & 1) ? e.x : at, valid > 1 && !(sure & 2) ? e.y : at,
                      valid > 2 && !(sure & 4) ? e.z : at, valid > 3 && !(sure & 8) ? e.w : at};
   float4 pf[4];
