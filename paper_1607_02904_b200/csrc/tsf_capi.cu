@@ -466,6 +466,66 @@ void get_state_device(Ctx& c, std::int64_t m, double* d_xyz, double* d_vel) {
 
 namespace {
 
+// Would evaluate() replay its graph now (so it can be captured inside a
+// larger graph as a child)?
+bool evaluate_replays(Ctx& c, tsf::Precision p, std::uint32_t flags) {
+  const int mode = int((flags & TSF_NO_FILTER) ? tsf::FilterMode::Copy : tsf::FilterMode::Pair);
+  const bool steady = !c.short_max_stale && c.short_apply == mode;
+  const std::uint64_t key[6] = {c.list_version, std::uint64_t(p),
+                                flags | (c.speculative ? 0x80000000u : 0u), std::uint64_t(c.n),
+                                std::uint64_t(c.n_owned),
+                                std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
+  const Ctx::GraphSlot& g = c.graph[0];
+  return graphs_enabled() && !c.graphs_off && !c.profile && steady && c.n > 0 && g.exec &&
+         std::equal(key, key + 6, g.key);
+}
+
+// An MD segment: replayed from graph slot 3 while its key holds, captured at
+// its first graphable run (segments repeat only within one list's life), else
+// launched eagerly.
+template <typename F>
+void run_segment(Ctx& c, const std::uint64_t* key, bool graphable, F&& launches) {
+  Ctx::GraphSlot& s = c.graph[3];
+  if (graphable && s.exec && std::equal(key, key + 6, s.key)) {
+    TSF_CUDA(cudaGraphLaunch(s.exec, c.stream));
+    c.launches += s.launches;
+    return;
+  }
+  if (!graphable) {
+    launches();
+    return;
+  }
+  if (s.exec) {
+    TSF_CUDA(cudaGraphExecDestroy(s.exec));
+    s.exec = nullptr;
+  }
+  const std::int64_t l0 = c.launches;
+  cudaGraph_t g = nullptr;
+  bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    try {
+      launches();
+    } catch (...) {
+      ok = false;
+    }
+    ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
+    ok = ok && cudaGraphInstantiate(&s.exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+  }
+  if (ok) {
+    s.launches = c.launches - l0;
+    std::copy(key, key + 6, s.key);
+    TSF_CUDA(cudaGraphLaunch(s.exec, c.stream));
+  } else {
+    cudaGetLastError();
+    if (s.exec) cudaGraphExecDestroy(s.exec);
+    s.exec = nullptr;
+    c.graphs_off = true;
+    c.launches = l0;
+    launches();
+  }
+}
+
 int compute_entry(tsf_ctx* ctx, tsf::Precision p, std::uint32_t flags, double* e, double* f,
                   double* w) {
   return guard(&ctx->c, [&] {
@@ -1104,31 +1164,63 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
       explicit Spec(Ctx& cc) : c(cc) { c.speculative = !c.profile; }
       ~Spec() { c.speculative = false; }
     } spec(c);
+    auto clear_moved = [&] {
+      TSF_CUDA(cudaMemsetAsync(c.flags.get() + tsf::kFlagMoved, 0, sizeof(int), c.stream));
+      TSF_CUDA(cudaMemsetAsync(c.flags.get() + tsf::kFlagMovedAny, 0, 2 * sizeof(int), c.stream));
+    };
+    clear_moved();
+    // Multi-step segments: up to TSF_MD_SEGMENT steps (default 8, never past
+    // a thermo sample) are queued — and, once the evaluation replays from its
+    // graph, captured and replayed as ONE graph — before the host looks at
+    // the flags.  A kick that moves an atom past skin/2 records its step;
+    // every later launch of the segment returns at once (k_reduce folds the
+    // step's flag into kFlagMovedAny, which the next kick reads), so the
+    // state stops at that step: the host rebuilds, re-evaluates it and
+    // resumes after it.
+    const char* seg_env = std::getenv("TSF_MD_SEGMENT");
+    const int seg_max = std::max(1, seg_env ? std::atoi(seg_env) : 8);
     bool kick_pending = false;
-    for (std::int64_t s = 1; s <= steps; ++s) {
-      // kick + drift + the rebuild test in one pass (flags[kFlagMoved])
-      tsf::md_kick(c, dt, true, kick_pending ? 2 : 1, /*check_rebuild=*/true);
-      TSF_CUDA(cudaMemcpyAsync(c.pinned_flag, c.flags.get() + tsf::kFlagMoved, sizeof(int),
-                               cudaMemcpyDeviceToHost, c.stream));
+    for (std::int64_t s = 1; s <= steps;) {
+      const std::int64_t sample_at =
+          std::min<std::int64_t>(steps, (s + thermo_every - 1) / thermo_every * thermo_every);
+      const std::int64_t e = std::min<std::int64_t>(sample_at, s + seg_max - 1);
+      const int first_kicks = kick_pending ? 2 : 1;
+      auto segment = [&] {
+        for (std::int64_t t = s; t <= e; ++t) {
+          tsf::md_kick(c, dt, true, t == s ? first_kicks : 2, /*check_rebuild=*/true, int(t - s));
+          evaluate(c, p, flags);
+        }
+      };
+      const std::uint64_t key[6] = {
+          c.list_version, std::uint64_t(p) | (std::uint64_t(e - s + 1) << 8) |
+                              (std::uint64_t(first_kicks) << 24),
+          flags | 0x80000000u, std::uint64_t(c.n), std::uint64_t(c.n_owned),
+          std::uint64_t(reinterpret_cast<std::uintptr_t>(c.stream))};
+      if (c.seg_dt != dt && c.graph[3].exec) {   // the kick nodes carry dt
+        TSF_CUDA(cudaGraphExecDestroy(c.graph[3].exec));
+        c.graph[3].exec = nullptr;
+      }
+      c.seg_dt = dt;
+      run_segment(c, key, c.speculative && evaluate_replays(c, p, flags), segment);
+      TSF_CUDA(cudaMemcpyAsync(c.pinned_flag, c.flags.get() + tsf::kFlagMovedAny,
+                               2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
       TSF_CUDA(cudaEventRecord(c.flag_event, c.stream));
-      if (c.speculative) evaluate(c, p, flags);
       TSF_CUDA(cudaEventSynchronize(c.flag_event));
-      if (*c.pinned_flag) {
-        // the speculative launches saw the flag and returned; clear it
-        // behind them so the re-evaluation runs
-        TSF_CUDA(cudaMemsetAsync(c.flags.get() + tsf::kFlagMoved, 0, sizeof(int), c.stream));
+      std::int64_t done = e;
+      if (c.pinned_flag[0]) {
+        // the segment stopped after the kick of step s + pinned_flag[1]
+        done = s + c.pinned_flag[1];
+        clear_moved();
         tsf::list_build(c, c.cutoff, c.skin);
         ++nreb;
         evaluate(c, p, flags);
-      } else if (!c.speculative) {
-        evaluate(c, p, flags);
       }
-      if (s % thermo_every == 0 || s == steps) {
+      kick_pending = true;
+      s = done + 1;
+      if (done == sample_at) {
         tsf::md_kick(c, dt, false);
-        sample(s);
+        sample(done);
         kick_pending = false;
-      } else {
-        kick_pending = true;
       }
     }
     if (nsamples) *nsamples = ns;

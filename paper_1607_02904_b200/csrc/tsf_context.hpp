@@ -73,6 +73,11 @@ constexpr int kFlagZero = 19;
 // NaN distances seen by a force-path filter (its own word: the filter's block 0
 // zeroes flags[0..3] while other blocks run); cleared when raised
 constexpr int kFlagFilterNaN = 20;
+// tsf_md_run's multi-step segments: the "moved" flag of any earlier step of
+// the segment (folded in by k_reduce, so it never changes during a kick) and
+// the step whose kick first set it
+constexpr int kFlagMovedAny = 21;
+constexpr int kFlagMovedStep = 22;
 
 struct ListState {
   int cap = 0;                 // ELL slots per atom
@@ -204,7 +209,8 @@ struct Ctx {
     std::int64_t launches = 0;         // kernels per replay
     int phase_blocks = 0;              // host state the launches leave behind
   };
-  GraphSlot graph[3];
+  GraphSlot graph[4];   // 0 evaluation, 1-2 split phases, 3 MD segment
+  double seg_dt = 0;    // time step baked into graph[3]'s kick nodes
   bool graphs_off = false;             // capture failed once: stay eager
 
   // MD state
@@ -273,7 +279,8 @@ void pack_velocities(Ctx& c);          // xyz_stage (user order velocities) -> v
 void unpack_velocities(Ctx& c);        // vel (slots) -> xyz_stage (user order)
 // v += F dt/(2 m mvv2e), `kicks` (1 or 2) times in a row [; x += v dt, wrap
 // [; the needs_rebuild test on the new positions -> flags[2]]]
-void md_kick(Ctx& c, double dt, bool drift, int kicks = 1, bool check_rebuild = false);
+void md_kick(Ctx& c, double dt, bool drift, int kicks = 1, bool check_rebuild = false,
+             int seg_step = -1);   // seg_step >= 0: a segment step (skips once a step moved)
 void md_kinetic(Ctx& c);               // KE -> result[7] (device)
 void md_scale_velocities(Ctx& c, double factor);
 

@@ -795,6 +795,8 @@ struct DomainDecomposition {
       TSF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned_flag), 64, cudaHostAllocDefault));
     if (!c->flag_event)
       TSF_CUDA(cudaEventCreateWithFlags(&c->flag_event, cudaEventDisableTiming));
+    TSF_CUDA(cudaMemsetAsync(c->flags.get() + kFlagMoved, 0, sizeof(int), s()));
+    TSF_CUDA(cudaMemsetAsync(c->flags.get() + kFlagMovedAny, 0, 2 * sizeof(int), s()));
     if (!c->forces_current) evaluate(p, flags);
     sample(0);
     struct Spec {
@@ -813,6 +815,7 @@ struct DomainDecomposition {
       TSF_CUDA(cudaEventSynchronize(c->flag_event));
       if (*c->pinned_flag) {
         TSF_CUDA(cudaMemsetAsync(c->flags.get() + kFlagMoved, 0, sizeof(int), s()));
+        TSF_CUDA(cudaMemsetAsync(c->flags.get() + kFlagMovedAny, 0, 2 * sizeof(int), s()));
         migrate();
         ++rb;
         ++rebuilds;

@@ -151,7 +151,7 @@ template <> struct Stage<float> {
 // A triplet that does not count enters with fck = dfck = 0 and ok = false:
 // every output is then exactly zero (the exponent argument is zeroed too, so
 // no inf can meet the zero), which replaces seven selects per triplet.
-template <typename R>
+template <typename R, bool EXPNB = false>
 __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R fck, R dfck,
                                            bool ok, const Row<R>& p) {
   Grad<R> o;
@@ -174,7 +174,8 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
 #if TSF_EXP_FIN >= 1
   const R ex = Fn<R>::exp_fin(cubic ? arg * arg * arg : arg);
 #else
-  const R ex = Fn<R>::exp_(cubic ? arg * arg * arg : arg);
+  const R ex = EXPNB ? Fn<R>::exp_nb(cubic ? arg * arg * arg : arg)
+                     : Fn<R>::exp_(cubic ? arg * arg * arg : arg);
 #endif
   const R gx = g * ex;
   o.z = fck * gx;
@@ -222,7 +223,8 @@ constexpr int kForceMinBlocks = G == 8 ? TSF_FORCE_MINB_F64_G8 : TSF_FORCE_MINB_
 template <int G>
 constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_FORCE_MINB_F32;
 
-template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FOREIGN = false>
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
+          bool EXPNB = false>
 __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     k_force(const __grid_constant__ ForceArgs<R> a) {
 #ifndef TSF_CACHE_G16
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
 
   griddep_wait();     // launch_pdl: the previous launch has completed
   griddep_launch();
-  if (a.skip && *a.skip) return;   // a speculative step whose list went stale
+  if (a.skip && (a.skip[0] | a.skip[kFlagMovedAny - kFlagMoved])) return;   // stale list
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   Acc e_acc = 0;
@@ -422,8 +424,10 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     const R fr = pjj.a * Fn<R>::exp_fin(-pjj.lam1 * me.r);
     const R fa = -(pjj.b * Fn<R>::exp_fin(-pjj.lam2 * me.r));
 #else
-    const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
-    const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
+    // (r <= 1 on empty slots, the pair cutoff otherwise: EXPNB's bound holds)
+    const R fr = pjj.a * (EXPNB ? Fn<R>::exp_nb(-pjj.lam1 * me.r) : Fn<R>::exp_(-pjj.lam1 * me.r));
+    const R fa = -(pjj.b * (EXPNB ? Fn<R>::exp_nb(-pjj.lam2 * me.r)
+                                  : Fn<R>::exp_(-pjj.lam2 * me.r)));
 #endif
     // meta: species of this slot as a k, or -1 when it can never be one.
     // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       }
       fck = ok ? fck : R(0);
       dfck = ok ? dfck : R(0);
-      const Grad<R> tr = triplet<R>(me, k, fck, dfck, ok, *prow);
+      const Grad<R> tr = triplet<R, EXPNB>(me, k, fck, dfck, ok, *prow);
       zeta += tr.z;
       gjx += tr.jx;
       gjy += tr.jy;
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         }
         fck = ok ? fck : R(0);
         dfck = ok ? dfck : R(0);
-        const Grad<R> tr = triplet<R>(me, k, fck, dfck, ok, *prow);
+        const Grad<R> tr = triplet<R, EXPNB>(me, k, fck, dfck, ok, *prow);
         sx = tr.kx * dvdz;
         sy = tr.ky * dvdz;
         sz = tr.kz * dvdz;
@@ -640,10 +644,13 @@ namespace {
 // step's critical path, and at 32k atoms it was a quarter of the step.
 static_assert(kRedWidth == 8, "k_reduce maps one quantity per thread mod 8");
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int nblocks,
-                                                double* __restrict__ out) {
+                                                double* __restrict__ out, int* __restrict__ fold) {
   __shared__ double s[32][kRedWidth];
   griddep_wait();
   const int t = threadIdx.x;
+  // speculative MD: this step's "moved" flag joins the segment's (one block,
+  // after every launch that reads both)
+  if (fold && t == 0 && fold[kFlagMoved]) fold[kFlagMovedAny] = 1;
   const int total = nblocks * kRedWidth;
   double acc = 0;
   for (int e = t; e < total; e += 1024) acc += partials[e];
@@ -751,6 +758,15 @@ Row<R> make_row(const Entry& e) {
   // bond-order series path (tsf_math.cuh): u < 2^-12 and |u / (2 eta)| < 2^-8
   r.lnu_fast = R(e.eta > 0 ? std::min(std::log(0x1p-12), std::log(0x1p-8 * 2.0 * e.eta))
                            : -1e300);
+  {
+    // every exp argument of a counted pair / triplet is bounded by the cutoff
+    // (r, r_ij, r_ik <= R + D): EXPNB's branch-free exp needs |x| < 708
+    const double cut = e.big_r + e.big_d;
+    const double tri = e.m == 3 ? std::pow(std::fabs(e.lambda3) * cut, 3.0)
+                                : std::fabs(e.lambda3) * cut;
+    r.exp_ok = R(tri < 700.0 && std::fabs(e.lambda1) * cut < 700.0 &&
+                         std::fabs(e.lambda2) * cut < 700.0 ? 1 : 0);
+  }
   r.gamma = R(e.gamma);
   r.gcd2 = R(e.gamma * c2 / d2);
   r.gc2 = R(e.gamma * c2);
@@ -791,6 +807,14 @@ template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN>
 int launch_main(Ctx& c, ForceArgs<R> a) {
   const int tiles = std::max(1, ceil_div(a.n_owned - a.slot_base, kBlock / G));
   auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN>;
+  // one species, FP64, G = 4: the branch-free exp when the row bounds every
+  // argument (Si: (lambda3 R)^3 = 76) — TSF_EXPNB=1 turns it on
+  if constexpr (SPEC == kSingle && G == 4 && std::is_same<R, double>::value) {
+    // measured slower (+6% on si2m: the interleaved chains spill): A/B only
+    const char* e = std::getenv("TSF_EXPNB");
+    if (a.row0.exp_ok != R(0) && e && e[0] == '1')
+      kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, true>;
+  }
   const int blocks = persistent_blocks(kern, tiles);
   c.mark(2);
   launch_pdl(kern, blocks, kBlock, c.stream, a);
@@ -919,7 +943,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     }
   }
   launch_pdl(k_reduce, 1, 1024, c.stream, static_cast<const double*>(c.partials.get()), nb,
-             c.result.get());
+             c.result.get(), c.speculative ? c.flags.get() : static_cast<int*>(nullptr));
   ++c.launches;
 }
 

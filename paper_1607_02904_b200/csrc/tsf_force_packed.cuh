@@ -22,6 +22,9 @@ namespace {
 #ifndef TSF_PACKED_SORT
 #define TSF_PACKED_SORT 1
 #endif
+#ifndef TSF_PACKED_STAGE
+#define TSF_PACKED_STAGE 0
+#endif
 #ifndef TSF_PACKED_CACHE_F64
 #define TSF_PACKED_CACHE_F64 5
 #endif
@@ -55,10 +58,17 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   __shared__ int s_cnt[kBlock];
   __shared__ int s_fgn[kBlock];
   __shared__ Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
+#if TSF_PACKED_STAGE
+  // the chunk's first 8 list entries and centre positions per atom, staged
+  // once per chunk (all 32 lanes' loads in flight together) instead of one
+  // dependent list -> position load chain per pack
+  __shared__ int4 s_list[kBlock][2];
+  __shared__ double4 s_posi[kBlock];
+#endif
 
   griddep_wait();
   griddep_launch();
-  if (a.skip && *a.skip) return;   // a speculative step whose list went stale
+  if (a.skip && (a.skip[0] | a.skip[kFlagMovedAny - kFlagMoved])) return;   // stale list
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int wbase = tid - lane;
@@ -86,13 +96,17 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   const bool has_ghosts = a.center_limit < a.n_owned;
   const bool has_foreign = FOREIGN && a.energy_limit < a.center_limit;
   const int items = OVF ? n_ovf : a.n_owned - a.slot_base;
-  const int chunks = (items + 31) / 32;
   const int nwarps = gridDim.x * (kBlock / 32);
+  // atoms per warp chunk: 32, or — a short queue (a few % of a crystal at
+  // 1600 K) — as few as 4 so that every warp of the launch takes a share
+  // instead of a handful of warps serialising six packs each
+  const int cw = OVF ? max(4, min(32, (items + nwarps - 1) / nwarps)) : 32;
+  const int chunks = (items + cw - 1) / cw;
 
   for (int chunk = blockIdx.x * (kBlock / 32) + tid / 32; chunk < chunks; chunk += nwarps) {
     // ---- this lane's atom of the chunk, its count, the warp scan ----
-    const int q = chunk * 32 + lane;
-    const bool in = q < items;
+    const int q = chunk * cw + lane;
+    const bool in = lane < cw && q < items;
     int i = in ? (OVF ? a.ovf_in[q] : a.slot_base + q) : 0;
     int n = in ? a.cnt[i] : 0;
     if (!OVF && has_ghosts && in && (a.perm ? a.perm[i] : i) >= a.center_limit) {
@@ -118,6 +132,14 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       f[0] = f[1] = f[2] = Acc(0);
     }
     int fgn = has_foreign && in && (a.perm ? a.perm[i] : i) >= a.energy_limit;
+#if TSF_PACKED_STAGE
+    if (n > 0) {
+      s_list[tid][0] = *reinterpret_cast<const int4*>(a.nbr + ell_at(0, i, a.npad));
+      if (n > 4) s_list[tid][1] = *reinterpret_cast<const int4*>(a.nbr + ell_at(4, i, a.npad));
+      s_posi[tid] = a.pos[i];
+    }
+    int orig = lane;                     // staging row of this lane's atom
+#endif
 #if TSF_PACKED_SORT
     {
       // order the chunk's atoms by count (bitonic, key (n, lane): unique, so
@@ -136,6 +158,9 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       i = __shfl_sync(kFull, i, src);
       n = __shfl_sync(kFull, n, src);
       fgn = __shfl_sync(kFull, fgn, src);
+#if TSF_PACKED_STAGE
+      orig = src;
+#endif
     }
 #endif
     int incl = n;
@@ -154,22 +179,49 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       if (mine) {
         s_atom[wbase + excl - base] = i;
         s_cnt[wbase + excl - base] = n;
+#if TSF_PACKED_STAGE
+        s_fgn[wbase + excl - base] = fgn | (orig << 1);
+#else
         s_fgn[wbase + excl - base] = fgn;
+#endif
       }
       __syncwarp();
       const bool slot = lane < used;
       const int h = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // bit 0 is set
       const int ai = s_atom[wbase + h];
       const int ni = slot ? s_cnt[wbase + h] : 0;
+#if TSF_PACKED_STAGE
+      const int hf = s_fgn[wbase + h];
+      const bool foreign = FOREIGN && (hf & 1);
+      const int orow = wbase + (hf >> 1);
+#else
       const bool foreign = FOREIGN && s_fgn[wbase + h];
+#endif
       const int gl = lane - h;
       TSF_DCHECK(h >= 0 && h <= lane && ai >= 0 && ai <= last, "k_force_packed segment head");
       TSF_DCHECK(!slot || (gl < ni && ni <= 32), "k_force_packed segment slot");
+#if TSF_PACKED_STAGE
+      int v = ai;
+      if (slot) {
+        if (gl < 8) {
+          const int4 e = s_list[orow][gl >> 2];
+          const int c = gl & 3;
+          v = c == 0 ? e.x : c == 1 ? e.y : c == 2 ? e.z : e.w;
+        } else {
+          v = a.nbr[ell_at(gl, ai, a.npad)];
+        }
+      }
+      TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
+      const int j = unsigned(v) <= unsigned(last) ? v : ai;
+      const double4 pi = s_posi[orow];
+      const double4 pj = a.pos[j];
+#else
       const int v = slot ? a.nbr[ell_at(gl, ai, a.npad)] : ai;
       TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
       const int j = unsigned(v) <= unsigned(last) ? v : ai;
       const double4 pi = a.pos[ai];
       const double4 pj = a.pos[j];
+#endif
 
       double dx = 0, dy = 0, dz = 0, r2 = 1.0;
       if (slot) {

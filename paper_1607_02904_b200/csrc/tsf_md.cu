@@ -146,8 +146,13 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        double dt, int drift, int kicks, Box box,
                        const double4* __restrict__ ref, double limit_sq,
                        int* __restrict__ moved_flag, const int* __restrict__ perm,
-                       int center_limit, const double4* __restrict__ dref) {
+                       int center_limit, const double4* __restrict__ dref,
+                       int* __restrict__ seg_flags, int seg_step) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  // a multi-step segment stops at the first step whose kick moved an atom
+  // past skin/2: later kicks leave the state as it was (the host rebuilds and
+  // resumes from that step)
+  if (seg_flags && seg_flags[kFlagMovedAny]) return;
   if (a >= n) return;
   // a decomposition's ghost copies are integrated by their owners and
   // refreshed by the forward exchange (center_limit < n only then)
@@ -184,8 +189,10 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
       displacement(ref[a], p, box, dx, dy, dz);
       const double d2 = norm_sq_exact(dx, dy, dz);
       const unsigned act = __activemask();
-      if (moved_flag && __any_sync(act, d2 > limit_sq) && (threadIdx.x & 31) == __ffs(act) - 1)
+      if (moved_flag && __any_sync(act, d2 > limit_sq) && (threadIdx.x & 31) == __ffs(act) - 1) {
         atomicOr(moved_flag, 1);
+        if (seg_flags) seg_flags[kFlagMovedStep] = seg_step;   // same value from every writer
+      }
       if (dref) {   // track_disp on the displacement just computed
         const int v = __reduce_max_sync(act, __float_as_int(__double2float_ru(d2)));
         if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(cmax + 5, v);
@@ -379,7 +386,7 @@ int center_limit(const Ctx& c) {   // user atoms below it are owned (all unless 
   return int(c.n_energy >= 0 ? std::min<std::int64_t>(c.n_energy, centers) : centers);
 }
 
-void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
+void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild, int seg_step) {
   if (c.n == 0) return;
   const bool check = drift && check_rebuild;
   if (check) TSF_CUDA(cudaMemsetAsync(c.flags.get() + kFlagMoved, 0, sizeof(int), c.stream));
@@ -387,7 +394,7 @@ void md_kick(Ctx& c, double dt, bool drift, int kicks, bool check_rebuild) {
       c.pos.get(), c.posf.get(), c.flags.get() + 5, c.vel.get(), c.forces.get(), int(c.n),
       masses_of(c), dt, drift ? 1 : 0, kicks, c.box, c.pos_ref.get(), 0.25 * c.skin * c.skin,
       check ? c.flags.get() + kFlagMoved : nullptr, c.sorted ? c.perm.get() : nullptr, center_limit(c),
-      disp_ref(c));
+      disp_ref(c), seg_step >= 0 ? c.flags.get() : nullptr, seg_step);
   ++c.launches;
 }
 

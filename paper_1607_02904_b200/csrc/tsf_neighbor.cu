@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     int zero_bytes, int slot_lo, int slot_hi, NearIn near, int* __restrict__ zero_flags) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
-  if (near.skip && *near.skip) return;   // a speculative step whose list went stale
+  // a speculative step whose list went stale (this step's kick, or an
+  // earlier step of a multi-step segment)
+  if (near.skip && (near.skip[0] | near.skip[kFlagMovedAny - kFlagMoved])) return;
   // error bits and tier queue counts of the force launches that follow
   if (zero_flags && blockIdx.x == 0 && threadIdx.x < 4) zero_flags[threadIdx.x] = 0;
   const int ns = pb.ns;

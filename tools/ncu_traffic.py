@@ -38,10 +38,14 @@ def fold(path):
         if kind == "force":
             # <R, Acc, G, SPEC, DET, OVF, FOREIGN>: only the main launch
             # (OVF = FOREIGN = 0), never a tier launch
-            lt = name.find("k_force<") + len("k_force<")
+            # packed: <R, Acc, SPEC, DET, OVF, FOREIGN>
+            packed = "k_force_packed<" in name
+            tag = "k_force_packed<" if packed else "k_force<"
+            lt = name.find(tag) + len(tag)
             args = [x.strip() for x in name[lt:name.find(">", lt)].split(",")]
-            if len(args) >= 7 and (args[5] not in ("0", "(bool)0", "false")
-                                   or args[6] not in ("0", "(bool)0", "false")):
+            o = 4 if packed else 5
+            if len(args) >= o + 2 and (args[o] not in ("0", "(bool)0", "false")
+                                       or args[o + 1] not in ("0", "(bool)0", "false")):
                 continue
         e = per.setdefault(d["ID"], {"kind": kind, "name": name})
         v = float(d["Metric Value"].replace(",", ""))
