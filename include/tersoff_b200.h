@@ -138,7 +138,9 @@ int tsf_compute_mixed(tsf_ctx* ctx, uint32_t flags, double* energy, double* forc
 int tsf_compute_f32(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
 
 /* One-shot drop-in: upload positions (and species/box), build the list when
- * it is missing or stale, evaluate, download.  precision: 0 f64, 1 mixed, 2 f32. */
+ * it is missing or stale, evaluate, download.  precision: 0 f64, 1 mixed, 2 f32.
+ * species may be NULL on a repeat call with the same n: the resident species
+ * stay (tsf_set_system accepts NULL species likewise). */
 int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xyz,
                         const int32_t* species, const double box[3], const uint8_t periodic[3],
                         double skin, uint32_t flags, double* energy, double* forces,

@@ -195,11 +195,21 @@ void set_system(Ctx& c, std::int64_t n, const double* xyz, const std::int32_t* s
   if (n < 0 || n > (std::int64_t(1) << 30)) throw tsf::ConfigError("atom count out of range");
   for (int ax = 0; ax < 3; ++ax)
     if (!(box[ax] > 0.0)) throw tsf::ConfigError("simulation box edges must be positive");
+  if (!species) {
+    // the resident species stay (repeat calls on the same system send only positions)
+    if (n != c.n || !c.species_set)
+      throw tsf::ConfigError("species may be NULL only when the context already holds the "
+                             "species of n atoms");
+    set_geometry(c, n, box, per);
+    upload_xyz(c, xyz);
+    return;
+  }
   // page-locked species go straight to the device and are validated there (no
   // O(n) host pass per call); pageable ones are checked and cached on the host
   const bool sp_pinned = n > 0 && is_pinned(species);
   if (!sp_pinned) check_species(c, n, species);
   set_geometry(c, n, box, per);
+  c.species_set = true;
   if (sp_pinned) {
     TSF_CUDA(cudaMemcpyAsync(c.species.get(), species, sizeof(int) * n, cudaMemcpyHostToDevice,
                              c.stream));
@@ -427,6 +437,7 @@ void set_system_device(Ctx& c, std::int64_t n, const double* d_xyz, const int* d
     if (!(box[ax] > 0.0)) throw ConfigError("simulation box edges must be positive");
   set_geometry(c, n, box, per);
   c.host_species.clear();
+  c.species_set = true;
   if (n == 0) return;
   TSF_CUDA(cudaMemcpyAsync(c.species.get(), d_species, sizeof(int) * n, cudaMemcpyDeviceToDevice,
                            c.stream));

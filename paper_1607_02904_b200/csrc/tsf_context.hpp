@@ -211,6 +211,7 @@ struct Ctx {
   };
   GraphSlot graph[4];   // 0 evaluation, 1-2 split phases, 3 MD segment
   double seg_dt = 0;    // time step baked into graph[3]'s kick nodes
+  bool species_set = false;   // species of the current n atoms are on the device
   bool graphs_off = false;             // capture failed once: stay eager
 
   // MD state

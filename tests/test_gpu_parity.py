@@ -478,3 +478,61 @@ def test_packed_lane_groups(tb, oracle, sic_text, monkeypatch, mode):
         e2, f2, w2 = ctx.compute("double", deterministic=True)
         assert e1 == e2 and np.array_equal(f1, f2) and np.array_equal(w1, w2)
         ctx.close()
+
+
+def test_asymmetric_cutoff_table(tb, oracle, sic_text):
+    """A LAMMPS-format table may give rows (i, *, k) and (k, *, i) different
+    cutoffs: here every Si-*-C row reaches 2.75 A and every
+    C-*-Si row 2.51 A, on a zincblende lattice stretched so the Si-C first
+    shell sits at 2.6 A.  The short-list bounds are symmetrised, so the
+    deterministic scatter (each atom gathers the slots of the centres in its
+    own list) and the atomics agree with the oracle."""
+    rows = []
+    for line in sic_text.splitlines():
+        t = line.split()
+        if len(t) == 17 and not line.lstrip().startswith("#"):
+            if t[0] == "Si" and t[2] == "C":
+                t[13], t[14] = "2.65", "0.10"          # R, D: cutoff 2.75
+            elif t[0] == "C" and t[2] == "Si":
+                t[13], t[14] = "2.41", "0.10"          # cutoff 2.51
+            line = " ".join(t)
+        rows.append(line)
+    text = "\n".join(rows) + "\n"
+    case = systems.zincblende(tb, text, 3, a0=6.0, jitter=0.12, seed=4, skin=0.5)
+    params, ctx = _ctx(tb, case)
+    _, _, _, ref = _oracle(oracle, case, params)
+    assert ref["energy"] != 0
+    for det in (True, False):
+        e, f, w = ctx.compute("double", deterministic=det)
+        assert abs(e - ref["energy"]) <= E_TOL_D * abs(ref["energy"]), det
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D, det
+    ctx.close()
+
+
+def test_evaluate_forces_resident_species(tb, oracle):
+    """tsf_evaluate_forces with species = NULL on a repeat call keeps the
+    resident species (the e2e path sends positions only); NULL before any
+    species were given is a ConfigError."""
+    import ctypes as C
+    from paper_1607_02904_b200 import _lib as L
+    case = systems.perturbed(tb, 3, 0.15, 8, skin=0.5)
+    params = tb.parse_params(case.params_text)
+    _, _, _, ref = _oracle(oracle, case, params)
+    lib = L.lib()
+    ctx = tb.Context(params, 0)
+    n = len(case.xyz)
+    xyz = np.ascontiguousarray(case.xyz)
+    box = np.ascontiguousarray(case.box, np.float64)
+    per = np.ascontiguousarray(case.periodic, np.uint8)
+    sp = np.ascontiguousarray(case.species, np.int32)
+    e = C.c_double()
+    f = np.zeros((n, 3))
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    assert lib.tsf_evaluate_forces(ctx._h, 0, n, vp(xyz), None, vp(box), vp(per), 0.5, 0,
+                                   C.byref(e), vp(f), None) == L.TSF_ERR_CONFIG
+    for species in (vp(sp), None, None):
+        assert lib.tsf_evaluate_forces(ctx._h, 0, n, vp(xyz), species, vp(box), vp(per), 0.5,
+                                       L.TSF_DETERMINISTIC, C.byref(e), vp(f), None) == 0
+        assert abs(e.value - ref["energy"]) <= E_TOL_D * abs(ref["energy"])
+        assert np.abs(f - ref["forces"]).max() <= F_TOL_D
+    ctx.close()
