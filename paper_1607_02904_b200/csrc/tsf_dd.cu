@@ -34,6 +34,8 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -97,9 +99,28 @@ struct NcclApi {
 const NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
+    // TSF_NCCL_LIB, else a libnccl the process already loaded (torch's, so one
+    // NCCL instance serves both), else the system's libnccl.so.2
+    std::string path;
+    if (const char* e = std::getenv("TSF_NCCL_LIB")) path = e;
+    if (path.empty()) {
+      if (std::FILE* f = std::fopen("/proc/self/maps", "r")) {
+        char line[4096];
+        while (std::fgets(line, sizeof line, f)) {
+          const char* p = std::strstr(line, "/");
+          if (p && std::strstr(p, "libnccl.so")) {
+            path = p;
+            while (!path.empty() && (path.back() == '\n' || path.back() == ' ')) path.pop_back();
+            break;
+          }
+        }
+        std::fclose(f);
+      }
+    }
+    if (!path.empty()) a.lib = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* nm : names)
-      if ((a.lib = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+      if (!a.lib) a.lib = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
     if (!a.lib) return a;
     a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.lib, "ncclGetUniqueId"));
     a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(a.lib, "ncclCommInitRank"));
