@@ -76,3 +76,28 @@ def test_run_nve_surface(tb):
     assert rep["csv"].startswith("step,time_ps,temp_K,pe_eV,ke_eV,etot_eV")
     assert rep["system"].natoms == 64
     assert abs(tb.temperature(s) - 300.0) <= 1e-9     # input untouched
+
+
+@pytest.mark.parametrize("segment", ["1", "3", "8"])
+def test_md_segments_are_bitwise_the_same_trajectory(tb, monkeypatch, segment):
+    """tsf_md_run's multi-step segments (TSF_MD_SEGMENT: steps queued or
+    graph-replayed per host check; a step that moves an atom past skin/2
+    stops the segment there) give bitwise the single-step loop's trajectory
+    and rebuild schedule in deterministic mode (3000 K: rebuilds every few
+    steps land inside segments)."""
+    def run(seg):
+        monkeypatch.setenv("TSF_MD_SEGMENT", seg)
+        s = _lattice(tb, 4, 3000.0, 77)
+        params = tb.builtin_silicon()
+        ctx = tb.Context(params, 0)
+        ctx.load(s)
+        ctx.build_neighbor_list(params.r_cut_max, 1.0)
+        ctx.md_set_state(s.velocities, s.species_masses)
+        thermo, reb = ctx.md_run(90, 0.001, "double", True, 30)
+        x, v = ctx.md_get_state()
+        ctx.close()
+        return thermo, reb, x, v
+    t1, r1, x1, v1 = run("1")
+    t2, r2, x2, v2 = run(segment)
+    assert r1 == r2 >= 3
+    assert np.array_equal(t1, t2) and np.array_equal(x1, x2) and np.array_equal(v1, v2)
