@@ -252,14 +252,13 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
 
       // partner of rotation t inside this lane's segment (itself once t >= n:
       // its triplet is masked and its k-gradient is zero)
-      auto triplet_at = [&](int t) {
+      auto triplet_at = [&](int t, Nbr<R>& k) {
         int m = gl;
         if (t < ni) {
           m = gl + t;
           if (m >= ni) m -= ni;
         }
         const int src = wbase + h + m;
-        Nbr<R> k;
         R fck, dfck, kmeta;
         st.get(src, k, fck, dfck, kmeta);
         bool ok = pair_ok && t < ni && kmeta >= R(0);
@@ -278,28 +277,30 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       };
 
       // ---- zeta pass ----
-      R zeta = 0, gjx = 0, gjy = 0, gjz = 0;
-      R ckx[kC + 1], cky[kC + 1], ckz[kC + 1];
+      // (k_force's scalar form: j-gradient u_j sum(B) + sum(u_k A), k-cache (C, D))
+      R zeta = 0, sb = 0, gjx = 0, gjy = 0, gjz = 0;
+      R ckc[kC + 1], ckd[kC + 1];
+      auto accumulate = [&](const Grad<R>& tr, const Nbr<R>& k) {
+        zeta += tr.z;
+        sb += tr.B;
+        gjx += k.ux * tr.A;
+        gjy += k.uy * tr.A;
+        gjz += k.uz * tr.A;
+      };
 #pragma unroll
       for (int t = 1; t <= kC; ++t) {
-        ckx[t] = cky[t] = ckz[t] = R(0);
+        ckc[t] = ckd[t] = R(0);
         if (t < tmax) {
-          const Grad<R> tr = triplet_at(t);
-          zeta += tr.z;
-          gjx += tr.jx;
-          gjy += tr.jy;
-          gjz += tr.jz;
-          ckx[t] = tr.kx;
-          cky[t] = tr.ky;
-          ckz[t] = tr.kz;
+          Nbr<R> k;
+          const Grad<R> tr = triplet_at(t, k);
+          accumulate(tr, k);
+          ckc[t] = tr.C;
+          ckd[t] = tr.D;
         }
       }
       for (int t = kC + 1; t < tmax; ++t) {
-        const Grad<R> tr = triplet_at(t);
-        zeta += tr.z;
-        gjx += tr.jx;
-        gjy += tr.jy;
-        gjz += tr.jz;
+        Nbr<R> k;
+        accumulate(triplet_at(t, k), k);
       }
 
       // ---- pair block ----
@@ -315,29 +316,38 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
         dvdz = R(0.5) * fc * fa * db;
         if (!isfinite(vv) || !isfinite(dvdr) || !isfinite(dvdz)) atomicOr(a.flags, kErrNonFinite);
       }
-      R px = -(me.ux * dvdr) - gjx * dvdz;
-      R py = -(me.uy * dvdr) - gjy * dvdz;
-      R pz = -(me.uz * dvdr) - gjz * dvdz;
+      R alpha = dvdr + dvdz * sb;
+      R px = -(gjx * dvdz);
+      R py = -(gjy * dvdz);
+      R pz = -(gjz * dvdz);
 
-      // ---- scatter: lane h + (gl - t) mod n sends its rotation-t k-gradient ----
-      auto receive = [&](int t, R sx, R sy, R sz) {
+      // ---- scatter: lane h + (gl - t) mod n sends its rotation-t (C, D) dV/dzeta ----
+      auto receive = [&](int t, R sc, R sd) {
         int s = gl;
         if (t < ni) {
           s = gl - t;
           if (s < 0) s += ni;
         }
         const int from = h + s;
-        px -= __shfl_sync(kFull, sx, from);
-        py -= __shfl_sync(kFull, sy, from);
-        pz -= __shfl_sync(kFull, sz, from);
+        const R rc = __shfl_sync(kFull, sc, from);
+        alpha += __shfl_sync(kFull, sd, from);
+        R sux, suy, suz;
+        st.unit(wbase + from, sux, suy, suz);
+        px -= sux * rc;
+        py -= suy * rc;
+        pz -= suz * rc;
       };
 #pragma unroll
       for (int t = 1; t <= kC; ++t)
-        if (t < tmax) receive(t, ckx[t] * dvdz, cky[t] * dvdz, ckz[t] * dvdz);
+        if (t < tmax) receive(t, ckc[t] * dvdz, ckd[t] * dvdz);
       for (int t = kC + 1; t < tmax; ++t) {
-        const Grad<R> tr = triplet_at(t);
-        receive(t, tr.kx * dvdz, tr.ky * dvdz, tr.kz * dvdz);
+        Nbr<R> k;
+        const Grad<R> tr = triplet_at(t, k);
+        receive(t, tr.C * dvdz, tr.D * dvdz);
       }
+      px -= me.ux * alpha;
+      py -= me.uy * alpha;
+      pz -= me.uz * alpha;
       if (!slot) px = py = pz = 0;
 
       // ---- F_i = -sum of the segment's P (and, queued + deterministic, the
