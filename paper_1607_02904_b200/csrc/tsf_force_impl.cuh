@@ -98,7 +98,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // Parameter-table specialisations.
 enum Spec : int {
-  kSingle = 0,   // one species: the row comes from the constant bank
+  kSingle = 0,   // one species, m = 3: the row comes from the constant bank
   kHoist = 1,    // several species, ramp (R, D) depends on (i, k) only
   kGeneric = 2,  // anything else: ramp and cutoff test per triplet
 };
@@ -166,7 +166,8 @@ template <> struct Stage<float> {
 // A triplet that does not count enters with fck = dfck = 0 and ok = false:
 // every output is then exactly zero (the exponent argument is zeroed too, so
 // no inf can meet the zero), which replaces seven selects per triplet.
-template <typename R, bool EXPNB = false>
+// CUB: 1 the exponent is cubic (m = 3), 0 linear, -1 read from the row.
+template <typename R, int CUB = -1, bool EXPNB = false>
 __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R fck, R dfck,
                                            bool ok, const Row<R>& p) {
   Grad<R> o;
@@ -184,17 +185,18 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
   const R iden = Fn<R>::rcp(den);
   const R g = p.gamma + p.gcd2 * (t * t) * iden;
   const R dg = R(-2) * p.gc2 * t * iden * iden;
-  const R arg = ok ? p.lam3 * (j.r - k.r) : R(0);
-  const bool cubic = p.m3 != R(0);
-#if TSF_EXP_FIN >= 1
-  const R ex = Fn<R>::exp_fin(cubic ? arg * arg * arg : arg);
-#else
-  const R ex = EXPNB ? Fn<R>::exp_nb(cubic ? arg * arg * arg : arg)
-                     : Fn<R>::exp_(cubic ? arg * arg * arg : arg);
-#endif
+  // e^{(lam3 q)^m} = exp_row(tc q^m), d/dq = td q^(m-1) e^{...} (make_row)
+  const R q = ok ? j.r - k.r : R(0);
+  const bool cubic = CUB > 0 || (CUB < 0 && p.m3 != R(0));
+  const R q2 = q * q;
+  const R x = cubic ? p.tc * (q2 * q) : p.tc * q;
+  R ex;
+  if constexpr (!std::is_same<R, double>::value) ex = Fn<R>::exp_row(x);   // base 2
+  else if constexpr (EXPNB) ex = Fn<R>::exp_nb(x);
+  else ex = TSF_EXP_FIN >= 1 ? Fn<R>::exp_fin(x) : Fn<R>::exp_(x);
   const R gx = g * ex;
   o.z = fck * gx;
-  const R fge = o.z * (cubic ? R(3) * p.lam3 * (arg * arg) : p.lam3);   // dz/dr_ij via exp
+  const R fge = o.z * (cubic ? p.td * q2 : p.td);                      // dz/dr_ij via exp
   const R fgd = fck * dg * ex;                                          // dz/dcos
   const R cge = dfck * gx;                                              // dz/dr_ik via f_C
   // dcos/dx_j = (u_k - u_j cos)/r_ij, dcos/dx_k = (u_j - u_k cos)/r_ik, folded:
@@ -431,15 +433,9 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     cutoff_ramp(me.r, pjj, fc, dfc);
     // the radial pair terms depend on r only: issued before the zeta pass so
     // their two exp chains overlap it instead of lengthening the pair block
-#if TSF_EXP_FIN >= 2
-    const R fr = pjj.a * Fn<R>::exp_fin(-pjj.lam1 * me.r);
-    const R fa = -(pjj.b * Fn<R>::exp_fin(-pjj.lam2 * me.r));
-#else
     // (r <= 1 on empty slots, the pair cutoff otherwise: EXPNB's bound holds)
-    const R fr = pjj.a * (EXPNB ? Fn<R>::exp_nb(-pjj.lam1 * me.r) : Fn<R>::exp_(-pjj.lam1 * me.r));
-    const R fa = -(pjj.b * (EXPNB ? Fn<R>::exp_nb(-pjj.lam2 * me.r)
-                                  : Fn<R>::exp_(-pjj.lam2 * me.r)));
-#endif
+    const R fr = pjj.a * (EXPNB ? Fn<R>::exp_nb(pjj.e1 * me.r) : Fn<R>::exp_row(pjj.e1 * me.r));
+    const R fa = -(pjj.b * (EXPNB ? Fn<R>::exp_nb(pjj.e2 * me.r) : Fn<R>::exp_row(pjj.e2 * me.r)));
     // meta: species of this slot as a k, or -1 when it can never be one.
     // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
     // exactly "pair (i, k) inside its own cutoff".
@@ -482,7 +478,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       }
       fck = ok ? fck : R(0);
       dfck = ok ? dfck : R(0);
-      const Grad<R> tr = triplet<R, EXPNB>(me, k, fck, dfck, ok, *prow);
+      const Grad<R> tr = triplet<R, (SPEC == kSingle ? 1 : -1), EXPNB>(me, k, fck, dfck, ok, *prow);
       zeta += tr.z;
       sb += tr.B;
       gjx += k.ux * tr.A;
@@ -547,7 +543,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         }
         fck = ok ? fck : R(0);
         dfck = ok ? dfck : R(0);
-        const Grad<R> tr = triplet<R, EXPNB>(me, k, fck, dfck, ok, *prow);
+        const Grad<R> tr = triplet<R, (SPEC == kSingle ? 1 : -1), EXPNB>(me, k, fck, dfck, ok, *prow);
         sc = tr.C * dvdz;
         sd = tr.D * dvdz;
       }
@@ -788,6 +784,15 @@ Row<R> make_row(const Entry& e) {
     r.exp_ok = R(tri < 700.0 && std::fabs(e.lambda1) * cut < 700.0 &&
                          std::fabs(e.lambda2) * cut < 700.0 ? 1 : 0);
   }
+  {
+    const double l2e = std::is_same<R, double>::value ? 1.0 : 1.4426950408889634;   // float: base 2
+    const double l3 = e.lambda3;
+    r.e1 = R(-e.lambda1 * l2e);
+    r.e2 = R(-e.lambda2 * l2e);
+    r.tc = R((e.m == 3 ? l3 * l3 * l3 : l3) * l2e);
+    r.td = R(e.m == 3 ? 3.0 * l3 * l3 * l3 : l3);
+    if (!std::is_same<R, double>::value) r.lnu_fast = R(double(r.lnu_fast) * l2e);   // log2 u
+  }
   r.gamma = R(e.gamma);
   r.gcd2 = R(e.gamma * c2 / d2);
   r.gc2 = R(e.gamma * c2);
@@ -976,7 +981,10 @@ void run_force(Ctx& c, const ForceArgs<R>& a) {
 
 template <typename R, typename Acc, bool DET>
 void dispatch_spec(Ctx& c, const ForceArgs<R>& a) {
-  if (c.params.species_count() == 1) run_force<R, Acc, kSingle, DET>(c, a);
+  // kSingle compiles the cubic triplet exponent in (every single-species
+  // table in use has m = 3); a single-species m = 1 table takes kHoist
+  if (c.params.species_count() == 1 && c.params.entry(0, 0, 0).m == 3)
+    run_force<R, Acc, kSingle, DET>(c, a);
   else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET>(c, a);
   else run_force<R, Acc, kGeneric, DET>(c, a);
 }

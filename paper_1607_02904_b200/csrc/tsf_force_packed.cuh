@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       me.uz = R(dz) * me.ir;
       R fc, dfc;
       cutoff_ramp(me.r, pjj, fc, dfc);
-      const R fr = pjj.a * Fn<R>::exp_(-pjj.lam1 * me.r);
-      const R fa = -(pjj.b * Fn<R>::exp_(-pjj.lam2 * me.r));
+      const R fr = pjj.a * Fn<R>::exp_row(pjj.e1 * me.r);
+      const R fa = -(pjj.b * Fn<R>::exp_row(pjj.e2 * me.r));
       const int meta = SPEC == kGeneric ? (slot ? sj : -1) : (pair_ok ? sj : -1);
       st.put(tid, me, fc, dfc, meta);
       if (SPEC == kGeneric) s_r2[tid] = r2;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
         }
         fck = ok ? fck : R(0);
         dfck = ok ? dfck : R(0);
-        return triplet<R>(me, k, fck, dfck, ok, *prow);
+        return triplet<R, (SPEC == kSingle ? 1 : -1)>(me, k, fck, dfck, ok, *prow);
       };
 
       // ---- zeta pass ----

@@ -30,17 +30,25 @@ def run(lib, cfg):
 
 
 def main():
-    a, b = sys.argv[1], sys.argv[2]
-    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-    cfgs = sys.argv[4:] or ["si2m"]
+    # ab.py <lib_a> <lib_b> [rounds] [config...], or
+    # ab.py --libs a,b,c[,...] [rounds] [config...] (any number of variants)
+    argv = sys.argv[1:]
+    if argv[0] == "--libs":
+        libs = argv[1].split(",")
+        argv = argv[2:]
+    else:
+        libs = argv[:2]
+        argv = argv[2:]
+    rounds = int(argv[0]) if argv else 3
+    cfgs = argv[1:] or ["si2m"]
     for cfg in cfgs:
-        res = {a: [], b: []}
+        res = {lib: [] for lib in libs}
         for _ in range(rounds):
-            for lib in (a, b):
+            for lib in libs:
                 res[lib].append(run(lib, cfg))
         for prec in ("double", "mixed", "single"):
             line = [cfg, prec]
-            for lib in (a, b):
+            for lib in libs:
                 step = statistics.median(r[prec][0] for r in res[lib])
                 kern = statistics.median(r[prec][1] for r in res[lib])
                 line.append(f"{os.path.basename(lib) or 'default'}: step {step:.4f} kernel {kern:.4f}")
