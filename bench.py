@@ -425,6 +425,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-md", action="store_true")
+    # the reference's evaluate_forces returns energy and forces only; the
+    # virial is this path's addition (A/B and forces-only workloads)
+    ap.add_argument("--no-virial", action="store_true",
+                    default=os.environ.get("TSF_BENCH_NO_VIRIAL") == "1")
     # the multi-GPU code path (GpuEngine + Decomposition) on one rank: a smoke
     # test of bench's N>1 branch where only one GPU is available
     ap.add_argument("--decompose", action="store_true")
@@ -461,7 +465,7 @@ def main():
 
         def step():
             ctx.compute(args.precision, deterministic=args.deterministic, energy=False,
-                        forces=False, virial=False)
+                        forces=False, virial=False, form_virial=not args.no_virial)
     else:
         # strong scaling: the same global system split into x slabs, one rank
         # per GPU, the C++ decomposition (csrc/tsf_dd.cu) over NCCL: ghost
@@ -649,7 +653,7 @@ def main():
         for prec in [p for p in DTYPES if p != args.precision]:
             def vstep(prec=prec):
                 ctx.compute(prec, deterministic=args.deterministic, energy=False, forces=False,
-                            virial=False)
+                            virial=False, form_virial=not args.no_virial)
             for _ in range(args.warmup):
                 vstep()
             torch.cuda.synchronize()

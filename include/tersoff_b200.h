@@ -41,6 +41,7 @@ extern "C" {
 /* compute flags */
 #define TSF_DETERMINISTIC 0x1u /* slot buffers + reverse gather: bitwise reproducible  */
 #define TSF_NO_FILTER 0x2u     /* ForceOptions::filter = false (potential_opt.hpp:35) */
+#define TSF_NO_VIRIAL 0x4u     /* the virial is not formed (result[1..6] stay zero)     */
 
 /* neighbor-list selectors for tsf_export_neighbors */
 #define TSF_LIST_SKIN 0  /* NeighborList (neighbor.hpp:15-27)              */
@@ -132,7 +133,11 @@ int tsf_export_neighbors(tsf_ctx* ctx, int which, int32_t* offsets, int32_t* nbr
  * mixed: float compute, double accumulation           (PrecisionMode::OptM)
  * f32:   float compute, float per-atom accumulation    (PrecisionMode::OptS)
  * Any of energy / forces (n*3) / virial (6: xx yy zz xy xz yz) may be NULL;
- * results then stay on the device and the call does not synchronize. */
+ * results then stay on the device and the call does not synchronize.  A NULL
+ * virial next to a non-NULL energy or forces skips the virial's arithmetic
+ * (the device copy, tsf_results_device, then holds zeros for it); with all
+ * three NULL everything is formed for tsf_results_device.  tsf_md_run and
+ * tsf_evaluate_forces with a NULL virial skip it likewise. */
 int tsf_compute_f64(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
 int tsf_compute_mixed(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
 int tsf_compute_f32(tsf_ctx* ctx, uint32_t flags, double* energy, double* forces, double* virial);
@@ -156,6 +161,10 @@ int tsf_math_probe(const tsf_params* p, int fn, int64_t n, const double* x, doub
 
 /* Kernel launches issued by this context since creation (evidence counter). */
 int64_t tsf_launch_count(const tsf_ctx* ctx);
+
+/* Near-list refreshes since creation (the filter rewrote both near lists from
+ * the skin list mid-life); synchronizes.  -1 on error. */
+int64_t tsf_near_refreshes(tsf_ctx* ctx);
 
 /* Per-stage CUDA-event timing of every evaluation while enabled (adds one
  * stream synchronization per evaluation).  ms[4] accumulates: filter, launch

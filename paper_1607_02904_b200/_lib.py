@@ -19,6 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 TSF_OK, TSF_ERR_INTERNAL, TSF_ERR_CONFIG, TSF_ERR_NUMERIC, TSF_ERR_CUDA = 0, 1, 2, 3, 4
 TSF_DETERMINISTIC = 0x1
 TSF_NO_FILTER = 0x2
+TSF_NO_VIRIAL = 0x4
 TSF_LIST_SKIN, TSF_LIST_SHORT = 0, 1
 
 _lock = threading.Lock()
@@ -84,6 +85,7 @@ PROTOTYPES = [
                                       C.c_uint32, _vp, _vp, _vp]),
     ("tsf_math_probe", C.c_int, [_vp, C.c_int, C.c_int64, _vp, _vp]),
     ("tsf_launch_count", C.c_int64, [_vp]),
+    ("tsf_near_refreshes", C.c_int64, [_vp]),
     ("tsf_profile_enable", C.c_int, [_vp, C.c_int]),
     ("tsf_profile_read", C.c_int, [_vp, _vp, _i64p, C.c_int]),
     ("tsf_set_stream", C.c_int, [_vp, _vp]),

@@ -344,6 +344,11 @@ class Context:
     def launches(self) -> int:
         return self._lib.tsf_launch_count(self._h)
 
+    @property
+    def near_refreshes(self) -> int:
+        """Near-list refreshes by the force-path filter since creation."""
+        return self._lib.tsf_near_refreshes(self._h)
+
     def profile(self, on: bool = True):
         self._ok(self._lib.tsf_profile_enable(self._h, int(on)))
 
@@ -412,14 +417,18 @@ class Context:
         return off, nb[:tot]
 
     def compute(self, precision="double", deterministic=False, filter=True, energy=True,
-                forces=True, virial=True):
+                forces=True, virial=True, form_virial=True):
         """Evaluate on the current system and list.  Returns (E, F, W) with
         None for outputs not requested; requesting nothing keeps the results on
-        the device and does not synchronize."""
+        the device and does not synchronize.  The virial is not formed when it
+        is not requested next to E or F, or when form_virial is False
+        (TSF_NO_VIRIAL: the device results then hold zeros for it)."""
         p = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
         fn = (self._lib.tsf_compute_f64, self._lib.tsf_compute_mixed,
               self._lib.tsf_compute_f32)[p]
         flags = (L.TSF_DETERMINISTIC if deterministic else 0) | (0 if filter else L.TSF_NO_FILTER)
+        if not form_virial:
+            flags |= L.TSF_NO_VIRIAL
         e = C.c_double(0.0)
         f = np.zeros((self.n, 3)) if forces else None
         w = np.zeros(6) if virial else None

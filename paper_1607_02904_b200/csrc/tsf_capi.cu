@@ -63,6 +63,7 @@ void DevBuf<T>::release() {
 
 template struct DevBuf<double>;
 template struct DevBuf<double4>;
+template struct DevBuf<float4>;
 template struct DevBuf<int>;
 template struct DevBuf<unsigned char>;
 template struct DevBuf<unsigned long long>;
@@ -539,6 +540,9 @@ void run_segment(Ctx& c, const std::uint64_t* key, bool graphable, F&& launches)
 
 int compute_entry(tsf_ctx* ctx, tsf::Precision p, std::uint32_t flags, double* e, double* f,
                   double* w) {
+  // outputs asked for without the virial: it is never formed.  (All three
+  // NULL: the caller reads the device results, virial included.)
+  if (!w && (e || f)) flags |= tsf::kFlagNoVirial;
   return guard(&ctx->c, [&] {
     evaluate(ctx->c, p, flags);
     finish(ctx->c, e, f, w);
@@ -680,9 +684,9 @@ int tsf_create(const tsf_params* p, int device, tsf_ctx** out) {
     c.device = device;
     TSF_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = c.stream;
-    c.flags.reserve(24);
+    c.flags.reserve(32);
     c.result.reserve(8);
-    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 24 * sizeof(int), c.stream));
+    TSF_CUDA(cudaMemsetAsync(c.flags.get(), 0, 32 * sizeof(int), c.stream));
     TSF_CUDA(cudaMemsetAsync(c.result.get(), 0, 8 * sizeof(double), c.stream));
     tsf::upload_params(c);
     c.masses.assign(std::size_t(c.params.species_count()), 28.0855);
@@ -856,6 +860,17 @@ int tsf_profile_read(tsf_ctx* ctx, double* ms, int64_t* calls, int reset) {
   });
 }
 int64_t tsf_launch_count(const tsf_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int64_t tsf_near_refreshes(tsf_ctx* ctx) {
+  if (!ctx) return -1;
+  int v = -1;
+  const int rc = guard(&ctx->c, [&] {
+    TSF_CUDA(cudaMemcpyAsync(&v, ctx->c.flags.get() + tsf::kFlagNearRefreshCount, sizeof(int),
+                             cudaMemcpyDeviceToHost, ctx->c.stream));
+    TSF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+  return rc == TSF_OK ? v : -1;
+}
 
 int tsf_set_system(tsf_ctx* ctx, int64_t n, const double* xyz, const int32_t* species,
                    const double box[3], const uint8_t periodic[3]) {
@@ -1045,7 +1060,7 @@ int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xy
     if (!c.skin_list.valid || c.skin != skin || c.cutoff != c.params.r_cut_max() ||
         tsf::list_needs_rebuild(c))
       tsf::list_build(c, c.params.r_cut_max(), skin);
-    evaluate(c, tsf::Precision(precision), flags);
+    evaluate(c, tsf::Precision(precision), virial ? flags : flags | tsf::kFlagNoVirial);
     finish(c, energy, forces, virial);
   });
 }
@@ -1140,6 +1155,7 @@ int tsf_md_run(tsf_ctx* ctx, int precision, int64_t steps, double dt, uint32_t f
     if (!c.skin_list.valid)
       throw tsf::ConfigError("no neighbor list: build one before running dynamics");
     const tsf::Precision p = tsf::Precision(precision);
+    flags |= tsf::kFlagNoVirial;   // thermo samples read energies only
     std::int64_t ns = 0, nreb = 0;
     auto sample = [&](std::int64_t step) {
       tsf::md_kinetic(c);

@@ -78,6 +78,10 @@ constexpr int kFlagFilterNaN = 20;
 // the step whose kick first set it
 constexpr int kFlagMovedAny = 21;
 constexpr int kFlagMovedStep = 22;
+// a filter launch refreshed the near lists (their displacement maximum,
+// flags[10], restarts: k_reduce clears both once every launch has read it)
+constexpr int kFlagNearRefresh = 23;
+constexpr int kFlagNearRefreshCount = 24;   // cumulative (tsf_near_refreshes)
 
 struct ListState {
   int cap = 0;                 // ELL slots per atom
@@ -139,6 +143,12 @@ struct Ctx {
   float near_t[2] = {0, 0};     // list q valid while |d|max^2 < near_t[q] = ((h_q - mu) / 2)^2
   int near_pre[2] = {4, 4};     // ELL4 blocks the filter requests up front from list q
   bool near_ok = false;
+  // Near-list refresh: when both near lists go stale mid-life, the force
+  // path's filter reads the skin list and writes both near lists afresh from
+  // the current positions; near_d0[s] keeps slot s's displacement since the
+  // build at that moment, so displacements are tracked from the refresh
+  // without a second position read (DispRef).
+  DevBuf<float4> near_d0;
   DevBuf<double> xyz_stage;    // AoS staging for H2D / D2H, user order
   DevBuf<double> forces;       // [n][3] slot order (accumulation, MD)
   DevBuf<double> forces_user;  // [n][3] user order (download)
@@ -255,6 +265,8 @@ enum class Precision { F64 = 0, Mixed = 1, F32 = 2 };
 constexpr std::uint32_t kFlagForcesZeroed = 1u << 16;
 // the filter launch zeroed flags[0..3] (error bits and tier queue counts)
 constexpr std::uint32_t kFlagFlagsZeroed = 1u << 17;
+// no caller reads this evaluation's virial (result[1..6] are left zero)
+constexpr std::uint32_t kFlagNoVirial = 0x4u;   // = TSF_NO_VIRIAL (include/tersoff_b200.h)
 void compute(Ctx& c, Precision prec, std::uint32_t flags);
 void upload_params(Ctx& c);
 

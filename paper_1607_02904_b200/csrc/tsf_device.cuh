@@ -127,16 +127,35 @@ __device__ __forceinline__ void track_coord_max(int* cmax, const double4& p) {
   if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(cmax, v);
 }
 
-// Largest squared displacement of a slot from its position at the last list
-// build (float bits rounded up, atomicMax; Ctx::near_list).  ref == nullptr: no list
-// of ours to track.  A NaN position propagates (its bits exceed +inf's), which
-// disables the filter's near-list path.
-__device__ __forceinline__ void track_disp(int* dmax, const double4* __restrict__ ref, int s,
+// The near lists' reference (Ctx::near_list): the positions at the last list
+// build (ref) and, per slot, the displacement from there at the last near-list
+// refresh (d0; zero after a build).  ref == nullptr: no list of ours to track.
+struct DispRef {
+  const double4* ref;
+  const float4* d0;
+};
+
+// |displacement since the near lists' reference|^2 from the displacement d
+// since the build: d - d0 (d0 is a float rounding of an exact displacement of
+// at most skin/2: its error, < 2^-25 A, lies far inside the lists' margin mu).
+__device__ __forceinline__ float near_disp2(const DispRef& r, int s, double dx, double dy,
+                                            double dz) {
+  const float4 o = r.d0[s];
+  dx -= double(o.x);
+  dy -= double(o.y);
+  dz -= double(o.z);
+  return __double2float_ru(norm_sq_exact(dx, dy, dz));
+}
+
+// Largest squared displacement of a slot since the near lists' reference
+// (float bits rounded up, atomicMax; Ctx::near_list).  A NaN position
+// propagates (its bits exceed +inf's), which disables the filter's near-list path.
+__device__ __forceinline__ void track_disp(int* dmax, const DispRef& r, int s,
                                            const double4& p, const Box& box) {
-  if (!ref) return;
+  if (!r.ref) return;
   double dx, dy, dz;
-  displacement(ref[s], p, box, dx, dy, dz);
-  const float d2 = __double2float_ru(norm_sq_exact(dx, dy, dz));
+  displacement(r.ref[s], p, box, dx, dy, dz);
+  const float d2 = near_disp2(r, s, dx, dy, dz);
   const unsigned act = __activemask();
   const int v = __reduce_max_sync(act, __float_as_int(d2));
   if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(dmax, v);

@@ -237,7 +237,7 @@ template <int G>
 constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_FORCE_MINB_F32;
 
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
-          bool EXPNB = false>
+          bool VIR = true, bool EXPNB = false>
 __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     k_force(const __grid_constant__ ForceArgs<R> a) {
 #ifndef TSF_CACHE_G16
@@ -591,13 +591,15 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     if (slot) {
       if constexpr (!(OVF && DET)) if (!FOREIGN || !foreign) {   // ghost centres: forces only
         e_acc += Acc(v);
-        const R rx = R(dx), ry = R(dy), rz = R(dz);
-        w_acc[0] += Acc(rx * px);
-        w_acc[1] += Acc(ry * py);
-        w_acc[2] += Acc(rz * pz);
-        w_acc[3] += Acc(rx * py);
-        w_acc[4] += Acc(rx * pz);
-        w_acc[5] += Acc(ry * pz);
+        if constexpr (VIR) {   // (no caller asked for the virial: not formed)
+          const R rx = R(dx), ry = R(dy), rz = R(dz);
+          w_acc[0] += Acc(rx * px);
+          w_acc[1] += Acc(ry * py);
+          w_acc[2] += Acc(rz * pz);
+          w_acc[3] += Acc(rx * py);
+          w_acc[4] += Acc(rx * pz);
+          w_acc[5] += Acc(ry * pz);
+        }
       }
       TSF_DCHECK(j >= 0 && j <= last && i >= 0 && i <= last, "k_force scatter target");
       if (DET) {
@@ -661,13 +663,21 @@ namespace {
 // step's critical path, and at 32k atoms it was a quarter of the step.
 static_assert(kRedWidth == 8, "k_reduce maps one quantity per thread mod 8");
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int nblocks,
-                                                double* __restrict__ out, int* __restrict__ fold) {
+                                                double* __restrict__ out, int* __restrict__ fold,
+                                                int* __restrict__ near_flags) {
   __shared__ double s[32][kRedWidth];
   griddep_wait();
   const int t = threadIdx.x;
   // speculative MD: this step's "moved" flag joins the segment's (one block,
   // after every launch that reads both)
   if (fold && t == 0 && fold[kFlagMoved]) fold[kFlagMovedAny] = 1;
+  // this evaluation's filter refreshed the near lists: the displacement
+  // maximum restarts from their new reference (every reader has run)
+  if (near_flags && t == 0 && near_flags[kFlagNearRefresh]) {
+    near_flags[kFlagNearRefresh] = 0;
+    near_flags[10] = 0;
+    ++near_flags[kFlagNearRefreshCount];
+  }
   const int total = nblocks * kRedWidth;
   double acc = 0;
   for (int e = t; e < total; e += 1024) acc += partials[e];
@@ -829,17 +839,17 @@ int persistent_blocks(K kernel, int tiles) {
 
 constexpr int kOverflowBlocks = 4 * 148;   // per tier launch; idle tiers exit at once
 
-template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN>
+template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN, bool VIR = true>
 int launch_main(Ctx& c, ForceArgs<R> a) {
   const int tiles = std::max(1, ceil_div(a.n_owned - a.slot_base, kBlock / G));
-  auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN>;
+  auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR>;
   // one species, FP64, G = 4: the branch-free exp when the row bounds every
   // argument (Si: (lambda3 R)^3 = 76) — TSF_EXPNB=1 turns it on
   if constexpr (SPEC == kSingle && G == 4 && std::is_same<R, double>::value) {
     // measured slower (+6% on si2m: the interleaved chains spill): A/B only
     const char* e = std::getenv("TSF_EXPNB");
     if (a.row0.exp_ok != R(0) && e && e[0] == '1')
-      kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, true>;
+      kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR, true>;
   }
   const int blocks = persistent_blocks(kern, tiles);
   c.mark(2);
@@ -860,10 +870,10 @@ int packed_over4_pct() {
   return e ? std::atoi(e) : 10;
 }
 
-template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN>
+template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN, bool VIR>
 int launch_main_packed(Ctx& c, ForceArgs<R> a) {
   const int chunks = std::max(1, ceil_div(a.n_owned - a.slot_base, 32));
-  auto kern = k_force_packed<R, Acc, SPEC, DET, false, FOREIGN>;
+  auto kern = k_force_packed<R, Acc, SPEC, DET, false, FOREIGN, VIR>;
   const int blocks = persistent_blocks(kern, ceil_div(chunks, kBlock / 32));
   c.mark(2);
   launch_pdl(kern, blocks, kBlock, c.stream, a);
@@ -872,7 +882,11 @@ int launch_main_packed(Ctx& c, ForceArgs<R> a) {
   return blocks;
 }
 
-template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN>
+// VIR = false: no caller reads the virial (the MD loop, evaluate_forces
+// without one, TSF_NO_VIRIAL) — the G = 4 and packed launches then never form
+// it (6 FP64 products per slot, 12 accumulator registers); the other widths,
+// rare, form it anyway.
+template <typename R, typename Acc, int SPEC, bool DET, bool FOREIGN, bool VIR>
 void run_force_t(Ctx& c, ForceArgs<R> a) {
   // Group width from the short-count distribution of the last list build
   // (atoms over 4 / over 8); atoms over the width — or that outgrow it
@@ -924,10 +938,10 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   int nb = c.phase_blocks;
   if (packed_main) {
     a.ovf_out = nullptr;
-    nb += launch_main_packed<R, Acc, SPEC, DET, FOREIGN>(c, a);
+    nb += launch_main_packed<R, Acc, SPEC, DET, FOREIGN, VIR>(c, a);
   } else {
     switch (g) {
-      case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN>(c, a); break;
+      case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN, VIR>(c, a); break;
       case 8: nb += launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
       case 16: nb += launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
       default: nb += launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
@@ -950,7 +964,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   if (pmode >= 1) {
     // one packed launch takes every queued atom, whatever its count
     if (g < 32)
-      tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN>,
+      tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN, VIR>,
            mx > g ? kOverflowBlocks : kOverflowBlocks / 4, true);
   } else {
     if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
@@ -969,29 +983,32 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     }
   }
   launch_pdl(k_reduce, 1, 1024, c.stream, static_cast<const double*>(c.partials.get()), nb,
-             c.result.get(), c.speculative ? c.flags.get() : static_cast<int*>(nullptr));
+             c.result.get(), c.speculative ? c.flags.get() : static_cast<int*>(nullptr),
+             c.near_ok ? c.flags.get() : static_cast<int*>(nullptr));
   ++c.launches;
 }
 
 template <typename R, typename Acc, int SPEC, bool DET>
-void run_force(Ctx& c, const ForceArgs<R>& a) {
-  if (a.energy_limit < a.center_limit) run_force_t<R, Acc, SPEC, DET, true>(c, a);
-  else run_force_t<R, Acc, SPEC, DET, false>(c, a);
+void run_force(Ctx& c, const ForceArgs<R>& a, bool vir) {
+  if (a.energy_limit < a.center_limit) run_force_t<R, Acc, SPEC, DET, true, true>(c, a);
+  else if (vir) run_force_t<R, Acc, SPEC, DET, false, true>(c, a);
+  else run_force_t<R, Acc, SPEC, DET, false, false>(c, a);
 }
 
 template <typename R, typename Acc, bool DET>
-void dispatch_spec(Ctx& c, const ForceArgs<R>& a) {
+void dispatch_spec(Ctx& c, const ForceArgs<R>& a, bool vir) {
   // kSingle compiles the cubic triplet exponent in (every single-species
   // table in use has m = 3); a single-species m = 1 table takes kHoist
   if (c.params.species_count() == 1 && c.params.entry(0, 0, 0).m == 3)
-    run_force<R, Acc, kSingle, DET>(c, a);
-  else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET>(c, a);
-  else run_force<R, Acc, kGeneric, DET>(c, a);
+    run_force<R, Acc, kSingle, DET>(c, a, vir);
+  else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET>(c, a, vir);
+  else run_force<R, Acc, kGeneric, DET>(c, a, vir);
 }
 
 template <typename R, typename Acc>
 void compute_t(Ctx& c, std::uint32_t flags) {
   const bool det = (flags & 0x1u) != 0;
+  const bool vir = !(flags & kFlagNoVirial);
   const std::size_t n = std::size_t(c.n);
   const int npad = c.npad;
   const int cap = c.short_list.cap;
@@ -1050,7 +1067,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     a.fself = c.fself.get();
     c.atom_ev.reserve(8 * n + 1);
     a.atom_ev = c.atom_ev.get();
-    dispatch_spec<R, Acc, true>(c, a);
+    dispatch_spec<R, Acc, true>(c, a, vir);
     if (n > 0 && c.phase_last) {
       k_gather<Acc><<<ceil_div(n, kBlock), kBlock, 0, c.stream>>>(
           int(n), npad, a.nbr, a.cnt, static_cast<const Acc*>(a.slot_x),
@@ -1069,7 +1086,7 @@ void compute_t(Ctx& c, std::uint32_t flags) {
     if (!(flags & kFlagForcesZeroed) && c.phase_first)
       TSF_CUDA(cudaMemsetAsync(target, 0, 3 * n * sizeof(Acc), c.stream));
     a.forces = target;
-    dispatch_spec<R, Acc, false>(c, a);
+    dispatch_spec<R, Acc, false>(c, a, vir);
     if (kF32 && n > 0 && c.phase_last) {
       k_to_double<<<ceil_div(3 * n, 256), 256, 0, c.stream>>>(
           reinterpret_cast<const float*>(target), c.forces.get(), 3 * n);

@@ -44,7 +44,8 @@ template <typename R>
 constexpr int kPackedMinBlocks =
     std::is_same<R, double>::value ? TSF_PACKED_MINB_F64 : TSF_PACKED_MINB_F32;
 
-template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN = false>
+template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
+          bool VIR = true>
 __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
     k_force_packed(const __grid_constant__ ForceArgs<R> a) {
   constexpr int kC = kPackedCacheRot<R>;
@@ -402,12 +403,14 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       if (slot) {
         if constexpr (!(OVF && DET)) if (!FOREIGN || !foreign) {
           e_acc += Acc(vv);
-          w_acc[0] += Acc(rx * px);
-          w_acc[1] += Acc(ry * py);
-          w_acc[2] += Acc(rz * pz);
-          w_acc[3] += Acc(rx * py);
-          w_acc[4] += Acc(rx * pz);
-          w_acc[5] += Acc(ry * pz);
+          if constexpr (VIR) {
+            w_acc[0] += Acc(rx * px);
+            w_acc[1] += Acc(ry * py);
+            w_acc[2] += Acc(rz * pz);
+            w_acc[3] += Acc(rx * py);
+            w_acc[4] += Acc(rx * pz);
+            w_acc[5] += Acc(ry * pz);
+          }
         }
         if (DET) {
           const std::size_t qs = std::size_t(gl) * a.npad + ai;

@@ -10,9 +10,11 @@ namespace {
 
 int blocks_for(std::int64_t n, int b = kBlock) { return int((n + b - 1) / b); }
 
-// the reference positions position writers track displacements against
-// (Ctx::near_list), or nullptr when no list of ours describes the slots
-const double4* disp_ref(const Ctx& c) { return c.near_ok ? c.pos_ref.get() : nullptr; }
+// the reference position writers track displacements against
+// (Ctx::near_list), ref = nullptr when no list of ours describes the slots
+DispRef disp_ref(const Ctx& c) {
+  return DispRef{c.near_ok ? c.pos_ref.get() : nullptr, c.near_d0.get()};
+}
 
 // slot s holds user atom perm[s] (perm == nullptr: identity)
 __device__ __forceinline__ int user_of(const int* __restrict__ perm, int s) {
@@ -26,7 +28,7 @@ __device__ __forceinline__ float4 shadow(const double4& p) {
 __global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ species,
                        const int* __restrict__ perm, int n, double4* __restrict__ pos,
                        float4* __restrict__ posf, int* __restrict__ cmax,
-                       const double4* __restrict__ dref, Box box) {
+                       DispRef dref, Box box) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int u = user_of(perm, s);
@@ -39,7 +41,7 @@ __global__ void k_pack(const double* __restrict__ xyz, const int* __restrict__ s
 
 __global__ void k_refresh_shadow(const double4* __restrict__ pos, int n,
                                  float4* __restrict__ posf, int* __restrict__ cmax,
-                                 const double4* __restrict__ dref, Box box) {
+                                 DispRef dref, Box box) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const double4 p = pos[s];
@@ -96,8 +98,7 @@ __global__ void k_gather_pos(const double4* __restrict__ pos, const int* __restr
 __global__ void k_scatter_pos(double4* __restrict__ pos, float4* __restrict__ posf,
                               int* __restrict__ cmax, const int* __restrict__ inv,
                               const int* __restrict__ species, int lo, int m,
-                              const double* __restrict__ in, const double4* __restrict__ dref,
-                              Box box) {
+                              const double* __restrict__ in, DispRef dref, Box box) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= m) return;
   const int s = slot_of(inv, lo + q);
@@ -146,7 +147,7 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
                        double dt, int drift, int kicks, Box box,
                        const double4* __restrict__ ref, double limit_sq,
                        int* __restrict__ moved_flag, const int* __restrict__ perm,
-                       int center_limit, const double4* __restrict__ dref,
+                       int center_limit, DispRef dref,
                        int* __restrict__ seg_flags, int seg_step) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   // a multi-step segment stops at the first step whose kick moved an atom
@@ -184,7 +185,7 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
     pos[a] = p;
     posf[a] = shadow(p);
     track_coord_max(cmax, p);
-    if (moved_flag || dref) {   // needs_rebuild (neighbor.cpp:134-141) on the new position
+    if (moved_flag || dref.ref) {   // needs_rebuild (neighbor.cpp:134-141) on the new position
       double dx, dy, dz;
       displacement(ref[a], p, box, dx, dy, dz);
       const double d2 = norm_sq_exact(dx, dy, dz);
@@ -193,8 +194,8 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
         atomicOr(moved_flag, 1);
         if (seg_flags) seg_flags[kFlagMovedStep] = seg_step;   // same value from every writer
       }
-      if (dref) {   // track_disp on the displacement just computed
-        const int v = __reduce_max_sync(act, __float_as_int(__double2float_ru(d2)));
+      if (dref.ref) {   // track_disp on the displacement just computed
+        const int v = __reduce_max_sync(act, __float_as_int(near_disp2(dref, a, dx, dy, dz)));
         if ((threadIdx.x & 31) == __ffs(act) - 1) lane_max(cmax + 5, v);
       }
     }

@@ -157,10 +157,19 @@ constexpr unsigned kSure = 0x80000000u;
 struct NearIn {
   const int* nbr[2];
   const int* cnt[2];
-  const int* dmax;   // squared displacement max since the build (float bits)
+  const int* dmax;   // squared displacement max since the near lists' reference (float bits)
   float t[2];
   int pre[2];
   const int* skip;   // speculative MD step: return at once when *skip != 0
+  // refresh (full-range force-path filters only; refresh = 0 elsewhere): with
+  // both lists stale the filter reads the skin list and rewrites both near
+  // lists (the lists above, written) and the reference displacements
+  int refresh;
+  double cut[2];       // near_cut[q]
+  double sure_cut[2];  // smallest pair bound - h_q
+  const double4* ref;  // build positions
+  float4* d0;          // per slot: displacement since the build at the refresh
+  int* refreshed;      // flags[kFlagNearRefresh]
 };
 
 // Skin list, one thread per slot: candidates are the stencil cells' slot
@@ -398,6 +407,27 @@ __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands&
 #pragma unroll
   for (int b = 0; b < 4; ++b)
     if (b < pre) e[b] = __ldcs(reinterpret_cast<const int4*>(L + ell_at(4 * b, at, a.npad)));
+  if (m <= 4 * pre) {
+    // every entry "sure" (a near list's usual case in a crystal): nothing to
+    // test, no shadow gather — the blocks go out with the bits stripped
+    bool all = true;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int v = m - 4 * b;
+      all = all && (b >= pre || ((v <= 0 || e[b].x < 0) && (v <= 1 || e[b].y < 0) &&
+                                 (v <= 2 || e[b].z < 0) && (v <= 3 || e[b].w < 0)));
+    }
+    if (all) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (b < pre && 4 * b < m) {
+          const int4 q = make_int4(e[b].x & 0x7fffffff, e[b].y & 0x7fffffff, e[b].z & 0x7fffffff,
+                                   e[b].w & 0x7fffffff);
+          *reinterpret_cast<int4*>(out + ell_at(4 * b, at, a.npad)) = q;
+        }
+      return m;
+    }
+  }
   // test all of them before any store or exact fallback: nothing between the
   // gathers keeps the compiler from issuing them back to back
   unsigned keep = 0, uns = 0;
@@ -435,6 +465,61 @@ __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands&
     if (un) k |= resolve_unsure<MULTI>(a, fb, L, at, s0, unsigned(un), unsigned(pr));
     keep_block(out, at, a.npad, q, int(k), w);
   }
+  return w;
+}
+
+// Near-list refresh (Ctx::near_d0): the short list from the skin list as
+// filter_list does, and both near lists rewritten on the same float r^2 — the
+// entries within near_cut[q] of the CURRENT positions, sure bits against
+// sure_cut[q] (k_skin_list's rules) — plus this slot's displacement since the
+// build, the new reference of the displacement maximum.  Valid by the build's
+// argument: any pair within a cutoff before the next rebuild is in the skin
+// list, and lies within r_cut_max + 2 |d|max of its distance now.
+template <bool MULTI>
+__device__ __forceinline__ int filter_refresh(const ListArgs& a, const FilterBands& fb,
+                                           const NearIn& near, int at,
+                                           const int* __restrict__ L, int m,
+                                           int* __restrict__ out) {
+  const float4 pfa = a.posf[at];
+  const int si = MULTI ? min(max(int(pfa.w), 0), fb.ns - 1) : 0;
+  float hi0, hi1, slo0, slo1, t;
+  band_for(near.cut[0], a.cmax, t, hi0);
+  band_for(near.cut[1], a.cmax, t, hi1);
+  band_for(fmax(near.sure_cut[0], 0.0), a.cmax, slo0, t);
+  band_for(fmax(near.sure_cut[1], 0.0), a.cmax, slo1, t);
+  int* n0 = const_cast<int*>(near.nbr[0]);
+  int* n1 = const_cast<int*>(near.nbr[1]);
+  int w = 0, w0 = 0, w1 = 0;
+  for (int s0 = 0; s0 < m; s0 += 4) {
+    const int4 q = __ldcs(reinterpret_cast<const int4*>(L + ell_at(s0, at, a.npad)));
+    const int e[4] = {q.x, q.y, q.z, q.w};
+    float4 pf[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pf[u] = a.posf[s0 + u < m ? e[u] : at];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (s0 + u >= m) continue;
+      const float r2 = dist2f(pfa, pf[u], fb.wrap);
+      const int pr = MULTI ? si * fb.ns + min(max(int(pf[u].w), 0), fb.ns - 1) : 0;
+      const float lo = MULTI ? fb.lo[pr] : fb.lo0, hi = MULTI ? fb.hi[pr] : fb.hi0;
+      bool in = r2 < lo;
+      if (!in && !(r2 > hi)) {
+        double dx, dy, dz;
+        displacement(a.pos[at], a.pos[e[u]], a.box, dx, dy, dz);
+        const double d2 = norm_sq_exact(dx, dy, dz);
+        in = d2 <= (MULTI ? fb.c2[pr] : fb.c20);
+        if (!in && fb.err && d2 != d2) atomicOr(fb.err + kFlagFilterNaN, 1);
+      }
+      if (in) out[ell_at(w++, at, a.npad)] = e[u];
+      if (!(r2 > hi0)) n0[ell_at(w0++, at, a.npad)] = int(unsigned(e[u]) | (r2 < slo0 ? kSure : 0u));
+      if (!(r2 > hi1)) n1[ell_at(w1++, at, a.npad)] = int(unsigned(e[u]) | (r2 < slo1 ? kSure : 0u));
+    }
+  }
+  const_cast<int*>(near.cnt[0])[at] = w0;
+  const_cast<int*>(near.cnt[1])[at] = w1;
+  double dx, dy, dz;
+  displacement(near.ref[at], a.pos[at], a.box, dx, dy, dz);
+  near.d0[at] = make_float4(float(dx), float(dy), float(dz), 0.0f);
   return w;
 }
 
@@ -476,20 +561,30 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
   const int* L = skin;
   const int* Lc = skin_cnt;
   int pre = 4;
+  bool refresh = false;
   if (near.nbr[0]) {
     const float d2 = __int_as_float(*near.dmax);
     const int q = d2 < near.t[0] ? 0 : d2 < near.t[1] ? 1 : 2;
     if (q < 2) {
-      L = near.nbr[q];
-      Lc = near.cnt[q];
-      pre = near.pre[q];
+      // selects, not an index: a run-time index into the parameter struct
+      // copies it to local memory in every thread
+      L = q == 0 ? near.nbr[0] : near.nbr[1];
+      Lc = q == 0 ? near.cnt[0] : near.cnt[1];
+      pre = q == 0 ? near.pre[0] : near.pre[1];
+    } else {
+      refresh = near.refresh != 0 && !(d2 != d2);   // grid-uniform
     }
   }
   const int m = Lc[at];
   int w = 0;
   if (apply) {
     const FilterBands fb{slo, shi, sc2, ns, slo[0], shi[0], sc2[0], wrap_of(a.boxf), zero_flags};
-    w = filter_list<MULTI>(a, fb, at, L, m, pre, out);
+    if (refresh) {
+      if (at == slot_lo) *near.refreshed = 1;
+      w = filter_refresh<MULTI>(a, fb, near, at, L, m, out);
+    } else {
+      w = filter_list<MULTI>(a, fb, at, L, m, pre, out);
+    }
   } else {
     for (int s = 0; s < m; ++s) out[ell_at(s, at, a.npad)] = skin[ell_at(s, at, a.npad)];
     w = m;
@@ -654,6 +749,13 @@ void launch_skin(Ctx& c, double bc2, int cap) {
               {c.near_cut[0] - rf, c.near_cut[1] - rf}},
       sure_bound(c, near));
   ++c.launches;
+}
+
+// TSF_NEAR_REFRESH=0: stale near lists fall back to the skin list (A/B; read
+// per eager filter launch, so tests can switch it)
+bool near_refresh_enabled() {
+  const char* e = std::getenv("TSF_NEAR_REFRESH");
+  return !(e && e[0] == '0');
 }
 
 int bits_for(std::int64_t v) {
@@ -839,10 +941,14 @@ void list_build(Ctx& c, double cutoff, double skin) {
 }
 
 void snapshot_reference_positions(Ctx& c) {
-  c.pos_ref.reserve(std::size_t(std::max<std::int64_t>(c.n, 1)));
+  const std::size_t nn = std::size_t(std::max<std::int64_t>(c.n, 1));
+  c.pos_ref.reserve(nn);
+  c.near_d0.reserve(nn);
   TSF_CUDA(cudaMemcpyAsync(c.pos_ref.get(), c.pos.get(), sizeof(double4) * c.n,
                            cudaMemcpyDeviceToDevice, c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.near_d0.get(), 0, sizeof(float4) * nn, c.stream));
   TSF_CUDA(cudaMemsetAsync(c.flags.get() + 10, 0, sizeof(int), c.stream));
+  TSF_CUDA(cudaMemsetAsync(c.flags.get() + kFlagNearRefresh, 0, sizeof(int), c.stream));
 }
 
 void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int lo, int hi,
@@ -863,13 +969,31 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
     // 2M atoms — its staging buffers take the L1 the position gathers hit,
     // 58% -> 9% hit rate)
     NearIn near{};
-    if (c.near_ok && mode != FilterMode::Copy)
-      near = NearIn{{c.near_list[0].nbr.get(), c.near_list[1].nbr.get()},
-                    {c.near_list[0].cnt.get(), c.near_list[1].cnt.get()},
-                    c.flags.get() + 10,
-                    {c.near_t[0], c.near_t[1]},
-                    {c.near_pre[0], c.near_pre[1]},
-                    nullptr};
+    if (c.near_ok && mode != FilterMode::Copy) {
+      near.nbr[0] = c.near_list[0].nbr.get();
+      near.nbr[1] = c.near_list[1].nbr.get();
+      near.cnt[0] = c.near_list[0].cnt.get();
+      near.cnt[1] = c.near_list[1].cnt.get();
+      near.dmax = c.flags.get() + 10;
+      near.t[0] = c.near_t[0];
+      near.t[1] = c.near_t[1];
+      near.pre[0] = c.near_pre[0];
+      near.pre[1] = c.near_pre[1];
+      // refresh only where a force launch (its k_reduce restarts the
+      // maximum) follows a filter over every slot: two-phase evaluations
+      // decide per phase and keep the stale-list fallback
+      near.refresh = mode == FilterMode::Pair && lo == 0 && hi == int(c.n) && zero_flags &&
+                     near_refresh_enabled();
+      const double rf = c.params.r_cut_max();
+      const PairBounds sb = sure_bound(c, true);
+      for (int q = 0; q < 2; ++q) {
+        near.cut[q] = c.near_cut[q];
+        near.sure_cut[q] = sb.cut[0] - (c.near_cut[q] - rf);
+      }
+      near.ref = c.pos_ref.get();
+      near.d0 = c.near_d0.get();
+      near.refreshed = c.flags.get() + kFlagNearRefresh;
+    }
     near.skip = c.speculative ? c.flags.get() + kFlagMoved : nullptr;
     (pb.ns > 1 ? k_filter<true> : k_filter<false>)<<<blocks_for(std::max(hi - lo, 1)), kBlock, 0,
                                                        c.stream>>>(

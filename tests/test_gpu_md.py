@@ -101,3 +101,31 @@ def test_md_segments_are_bitwise_the_same_trajectory(tb, monkeypatch, segment):
     t2, r2, x2, v2 = run(segment)
     assert r1 == r2 >= 3
     assert np.array_equal(t1, t2) and np.array_equal(x1, x2) and np.array_equal(v1, v2)
+
+
+@pytest.mark.parametrize("precision", ["double", "mixed"])
+def test_near_list_refresh_is_bitwise_the_same_trajectory(tb, monkeypatch, precision):
+    """Near-list refresh: when both near lists go stale the
+    force-path filter rewrites them from the skin list and restarts the
+    displacement maximum from there.  The short list it hands the force
+    kernel is the same subsequence of the skin list either way, so the
+    deterministic trajectory, thermo and rebuild schedule are bitwise those of
+    the skin-list fallback (TSF_NEAR_REFRESH=0) — and refreshes did happen."""
+    def run(flag):
+        monkeypatch.setenv("TSF_NEAR_REFRESH", flag)
+        s = _lattice(tb, 6, 1600.0, 4242)
+        params = tb.builtin_silicon()
+        ctx = tb.Context(params, 0)
+        ctx.load(s)
+        ctx.build_neighbor_list(params.r_cut_max, 1.0)
+        ctx.md_set_state(s.velocities, s.species_masses)
+        thermo, reb = ctx.md_run(160, 0.001, precision, True, 40)
+        x, v = ctx.md_get_state()
+        refreshes = ctx.near_refreshes
+        ctx.close()
+        return thermo, reb, x, v, refreshes
+    t0, r0, x0, v0, n0 = run("0")
+    t1, r1, x1, v1, n1 = run("1")
+    assert n0 == 0 and n1 >= 2
+    assert r0 == r1 >= 3
+    assert np.array_equal(t0, t1) and np.array_equal(x0, x1) and np.array_equal(v0, v1)

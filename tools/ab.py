@@ -2,7 +2,7 @@
 `TSF_LIBRARY=<a>` / `<b>` bench runs (device-resident, all precisions as
 variants) R times and print the median kernel and step times per config.
 usage: python tools/ab.py <lib_a> <lib_b> [rounds] [config...]
-(a "lib" may also be "+NAME=VALUE": the default library with that env setting)"""
+(a "lib" may carry env settings: "path+NAME=VALUE", "+NAME=VALUE" for the default library)"""
 import json
 import os
 import statistics
@@ -14,11 +14,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def run(lib, cfg):
     # lib: a library path, or "+NAME=VALUE" (the default library with an env setting)
-    if lib.startswith("+"):
-        k, v = lib[1:].split("=", 1)
-        env = dict(os.environ, **{k: v})
-    else:
-        env = dict(os.environ, TSF_LIBRARY=lib) if lib else dict(os.environ)
+    # "path+NAME=VALUE+NAME2=VALUE2": a library (empty: the default) with env settings
+    path, *sets = lib.split("+")
+    env = dict(os.environ, TSF_LIBRARY=path) if path else dict(os.environ)
+    for kv in sets:
+        k, v = kv.split("=", 1)
+        env[k] = v
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg,
                           "--steps", "300", "--no-cpu-baseline", "--no-e2e"],
                          capture_output=True, text=True, env=env, timeout=600)
@@ -26,6 +27,8 @@ def run(lib, cfg):
     r = {"double": (d["ms_per_step"], d["roofline"]["kernel_ms"])}
     for p, v in d["variants"].items():
         r[p] = (v["ms_per_step"], v["kernel_ms"])
+    if d.get("md"):
+        r["md"] = (d["md"]["ms_per_step"], d["md"]["ms_per_step"])
     return r
 
 
@@ -46,7 +49,7 @@ def main():
         for _ in range(rounds):
             for lib in libs:
                 res[lib].append(run(lib, cfg))
-        for prec in ("double", "mixed", "single"):
+        for prec in [p for p in ("double", "mixed", "single", "md") if p in res[libs[0]][0]]:
             line = [cfg, prec]
             for lib in libs:
                 step = statistics.median(r[prec][0] for r in res[lib])
