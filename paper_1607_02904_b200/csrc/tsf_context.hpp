@@ -82,6 +82,9 @@ constexpr int kFlagMovedStep = 22;
 // flags[10], restarts: k_reduce clears both once every launch has read it)
 constexpr int kFlagNearRefresh = 23;
 constexpr int kFlagNearRefreshCount = 24;   // cumulative (tsf_near_refreshes)
+// a force-path filter saw a short count over 4 (set once, check before store;
+// cleared by k_reduce): an idle packed tier launch exits without scanning
+constexpr int kFlagOver4 = 25;
 
 struct ListState {
   int cap = 0;                 // ELL slots per atom
@@ -205,6 +208,8 @@ struct Ctx {
   // once when flags[kFlagMoved] is set (the step is then re-evaluated after
   // the rebuild), so the GPU never waits for the host between steps
   bool speculative = false;
+  bool filter_marks_over4 = false;   // the last filter launch raised flags[kFlagOver4]
+  bool main_packed = false;          // the last force evaluation's main launch was packed
   int* pinned_flag = nullptr;          // page-locked host word for the flag readback
   cudaEvent_t flag_event = nullptr;
   // identity of the externally supplied list on the device (tsf_set_neighbor_list)

@@ -78,8 +78,13 @@ struct ForceArgs {
   // wider tier launch (main G=4/8 -> G=16 -> G=32); the last tier flags them.
   const int* ovf_in;        // tier launches: queued slots and their count
   const int* ovf_in_count;
-  int* ovf_out;             // nullptr: more than G entries is an error
+  int* ovf_out;             // nullptr: more than G entries is an error (unless ovf_scan)
   int* ovf_out_count;
+  // ovf_scan: the main launch leaves atoms over its width to a packed tier
+  // launch that finds them itself (short count > scan_g) — no queue
+  int ovf_scan;
+  int scan_g;
+  const int* over4;         // scanning tier: flags[kFlagOver4] (nullptr: always scan)
   double* atom_ev;          // deterministic tiers: per-atom energy + virial [n][8]
   int* flags;               // [0] error bits
   const int* skip;          // speculative MD step: return at once when *skip != 0
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     // per-atom form (tools/ab.py: the vote cost the float G = 4 kernel 1%).
     if constexpr ((G == 4 && std::is_same<R, double>::value) || OVF) {
       const bool over = n_i > G;
-      const unsigned lead = __ballot_sync(kFull, over && gl == 0);
+      const unsigned lead = a.ovf_scan ? 0u : __ballot_sync(kFull, over && gl == 0);
       if (lead) {                      // warp-uniform
         if (a.ovf_out) {
           const int first = __ffs(lead) - 1;
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       }
     } else {
       if (n_i > G) {
-        if (gl == 0) {
+        if (gl == 0 && !a.ovf_scan) {
           if (a.ovf_out) a.ovf_out[atomicAdd(a.ovf_out_count, 1)] = i;
           else atomicOr(a.flags, kErrShortOverflow);
         }
@@ -664,7 +669,8 @@ namespace {
 static_assert(kRedWidth == 8, "k_reduce maps one quantity per thread mod 8");
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ partials, int nblocks,
                                                 double* __restrict__ out, int* __restrict__ fold,
-                                                int* __restrict__ near_flags) {
+                                                int* __restrict__ near_flags,
+                                                int* __restrict__ over4) {
   __shared__ double s[32][kRedWidth];
   griddep_wait();
   const int t = threadIdx.x;
@@ -673,6 +679,7 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
   if (fold && t == 0 && fold[kFlagMoved]) fold[kFlagMovedAny] = 1;
   // this evaluation's filter refreshed the near lists: the displacement
   // maximum restarts from their new reference (every reader has run)
+  if (over4 && t == 0) *over4 = 0;   // the tier has read it
   if (near_flags && t == 0 && near_flags[kFlagNearRefresh]) {
     near_flags[kFlagNearRefresh] = 0;
     near_flags[10] = 0;
@@ -706,7 +713,7 @@ __global__ void __launch_bounds__(kBlock) k_queued_ev(const double* __restrict__
   __shared__ double s[kBlock][7];
   const int t = threadIdx.x;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  if (*queued > 0) {
+  if (!queued || *queued > 0) {   // (no count: a scanning tier took them)
     const int chunk = (n_owned + gridDim.x - 1) / gridDim.x;
     const int lo = blockIdx.x * chunk, hi = min(n_owned, lo + chunk);
     for (int i = lo + t; i < hi; i += kBlock)
@@ -920,6 +927,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
       !(pinned == 4 || pinned == 8 || pinned == 16 || pinned == 32) && pmode >= 1 &&
       (pmode == 2 || (mx > 4 && s.over4 * 100 > packed_over4_pct() * n));
   if (packed_main) g = 32;
+  c.main_packed = packed_main;
   // Tier chain: atoms over the main width are queued for G = 8 (when the
   // last rebuild saw counts over 4), then G = 16 (counts over 8), then
   // G = 32, which takes whatever is left — including atoms that outgrew the
@@ -932,6 +940,10 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   int cur = 0;                              // queue the main launch fills
   a.ovf_out = g < 32 ? qbuf : nullptr;
   a.ovf_out_count = a.flags + 1;
+  // packed tier (default): the main launch queues nothing, the tier scans
+  a.ovf_scan = pmode >= 1 && g < 32 ? 1 : 0;
+  a.scan_g = g;
+  a.over4 = c.filter_marks_over4 && c.phase_first ? a.flags + kFlagOver4 : nullptr;
   // two-phase evaluation: the partials of the first phase's main launch
   // precede this one's; tiers and the reduction run with the last phase
   a.partial_base = c.phase_blocks;
@@ -962,10 +974,15 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     if (!last) ++cur;
   };
   if (pmode >= 1) {
-    // one packed launch takes every queued atom, whatever its count
-    if (g < 32)
-      tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN, VIR>,
-           mx > g ? kOverflowBlocks : kOverflowBlocks / 4, true);
+    // one packed launch takes every queued atom, whatever its count.  Full
+    // occupancy whatever the last rebuild saw: the queue grows between
+    // rebuilds (Si at 1600 K: 0 -> 180k atoms with a 5th neighbour within 60
+    // fs of a rebuild), and a quarter grid left 4 warps per SM to serialise
+    // it (0.2 ms); an empty queue exits at once either way
+    if (g < 32) {
+      a.slot_base = 0;                      // every phase's slots
+      tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN, VIR>, kOverflowBlocks, true);
+    }
   } else {
     if (g < 8 && mx > 4) tier(k_force<R, Acc, 8, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
     if (g < 16 && mx > 8) tier(k_force<R, Acc, 16, SPEC, DET, true, FOREIGN>, kOverflowBlocks, false);
@@ -976,7 +993,8 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   if (g < 32) {
     if (DET) {
       k_queued_ev<<<kOverflowBlocks, kBlock, 0, c.stream>>>(
-          a.atom_ev, a.cnt, a.perm, a.n_owned, a.energy_limit, g, a.flags + 1,
+          a.atom_ev, a.cnt, a.perm, a.n_owned, a.energy_limit, g,
+          a.ovf_scan ? static_cast<const int*>(nullptr) : a.flags + 1,
           a.partials + std::size_t(nb) * kRedWidth);
       nb += kOverflowBlocks;
       ++c.launches;
@@ -984,7 +1002,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   }
   launch_pdl(k_reduce, 1, 1024, c.stream, static_cast<const double*>(c.partials.get()), nb,
              c.result.get(), c.speculative ? c.flags.get() : static_cast<int*>(nullptr),
-             c.near_ok ? c.flags.get() : static_cast<int*>(nullptr));
+             c.near_ok ? c.flags.get() : static_cast<int*>(nullptr), c.flags.get() + kFlagOver4);
   ++c.launches;
 }
 

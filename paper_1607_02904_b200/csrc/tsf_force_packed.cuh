@@ -4,8 +4,10 @@
 // k_force gives every central atom a power-of-two group of G lanes, so an
 // atom with 5 short neighbours idles 3 lanes of a G = 8 group, and an
 // irregular system (3C-SiC: 45% of the atoms over 4; the 3000 K liquid: 2..13)
-// either idles lanes or queues atoms to wider tier launches.  Here a warp
-// takes a chunk of 32 consecutive atoms (or queued atoms), scans their short
+// either idles lanes or leaves atoms to wider launches.  Here a warp takes a
+// chunk of 32 atoms — consecutive slots (main launch), or, behind a G-wide
+// main launch, the next 32 atoms over G of its own slot range (tier launch:
+// found by scanning the counts, no queue) — sorts them by count, scans the
 // counts and packs their neighbour slots back to back: a pack is the longest
 // run of atoms whose slots fit in 32 lanes, segment heads come from a ballot,
 // every lane finds its atom through its segment head, and the rotation scheme
@@ -21,9 +23,6 @@ namespace {
 
 #ifndef TSF_PACKED_SORT
 #define TSF_PACKED_SORT 1
-#endif
-#ifndef TSF_PACKED_STAGE
-#define TSF_PACKED_STAGE 0
 #endif
 #ifndef TSF_PACKED_CACHE_F64
 #define TSF_PACKED_CACHE_F64 5
@@ -59,13 +58,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   __shared__ int s_cnt[kBlock];
   __shared__ int s_fgn[kBlock];
   __shared__ Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
-#if TSF_PACKED_STAGE
-  // the chunk's first 8 list entries and centre positions per atom, staged
-  // once per chunk (all 32 lanes' loads in flight together) instead of one
-  // dependent list -> position load chain per pack
-  __shared__ int4 s_list[kBlock][2];
-  __shared__ double4 s_posi[kBlock];
-#endif
+  __shared__ int s_buf[OVF ? kBlock / 32 : 1][128];   // scanning tier: slots, counts
 
   griddep_wait();
   griddep_launch();
@@ -76,12 +69,6 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   Acc e_acc = 0;
   Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
 
-  const int n_ovf = OVF ? *a.ovf_in_count : 0;
-  if (OVF && n_ovf == 0) {
-    if (tid < kRedWidth)
-      a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
-    return;
-  }
   const int ns = a.ns;
   const Row<R>* rows = static_cast<const Row<R>*>(a.rows);
   const Row<R>& row0 = a.row0;
@@ -96,51 +83,12 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   const int last = a.n_all - 1;
   const bool has_ghosts = a.center_limit < a.n_owned;
   const bool has_foreign = FOREIGN && a.energy_limit < a.center_limit;
-  const int items = OVF ? n_ovf : a.n_owned - a.slot_base;
   const int nwarps = gridDim.x * (kBlock / 32);
-  // atoms per warp chunk: 32, or — a short queue (a few % of a crystal at
-  // 1600 K) — as few as 4 so that every warp of the launch takes a share
-  // instead of a handful of warps serialising six packs each
-  const int cw = OVF ? max(4, min(32, (items + nwarps - 1) / nwarps)) : 32;
-  const int chunks = (items + cw - 1) / cw;
+  const int warp = blockIdx.x * (kBlock / 32) + tid / 32;
 
-  for (int chunk = blockIdx.x * (kBlock / 32) + tid / 32; chunk < chunks; chunk += nwarps) {
-    // ---- this lane's atom of the chunk, its count, the warp scan ----
-    const int q = chunk * cw + lane;
-    const bool in = lane < cw && q < items;
-    int i = in ? (OVF ? a.ovf_in[q] : a.slot_base + q) : 0;
-    int n = in ? a.cnt[i] : 0;
-    if (!OVF && has_ghosts && in && (a.perm ? a.perm[i] : i) >= a.center_limit) {
-      // a decomposition ghost copy: receives forces, is not a centre
-      if (DET) {   // zero its self term and the slots k_gather reads
-        Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
-        f[0] = f[1] = f[2] = Acc(0);
-        for (int sl = 0; sl < n; ++sl) {
-          const std::size_t qs = std::size_t(sl) * a.npad + i;
-          static_cast<Acc*>(a.slot_x)[qs] = Acc(0);
-          static_cast<Acc*>(a.slot_y)[qs] = Acc(0);
-          static_cast<Acc*>(a.slot_z)[qs] = Acc(0);
-        }
-      }
-      n = 0;
-    }
-    if (n > 32) {                        // no wider launch behind this one
-      atomicOr(a.flags, kErrShortOverflow);
-      n = 0;
-    }
-    if (DET && in && n == 0) {           // no segment, no head: F_self = 0 here
-      Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
-      f[0] = f[1] = f[2] = Acc(0);
-    }
-    int fgn = has_foreign && in && (a.perm ? a.perm[i] : i) >= a.energy_limit;
-#if TSF_PACKED_STAGE
-    if (n > 0) {
-      s_list[tid][0] = *reinterpret_cast<const int4*>(a.nbr + ell_at(0, i, a.npad));
-      if (n > 4) s_list[tid][1] = *reinterpret_cast<const int4*>(a.nbr + ell_at(4, i, a.npad));
-      s_posi[tid] = a.pos[i];
-    }
-    int orig = lane;                     // staging row of this lane's atom
-#endif
+  // One chunk: this lane's atom i (slot) with short count n (0: none) and its
+  // ghost-centre bit; the warp sorts, scans and packs the chunk's slots.
+  auto chunk_body = [&](int i, int n, int fgn) {
 #if TSF_PACKED_SORT
     {
       // order the chunk's atoms by count (bitonic, key (n, lane): unique, so
@@ -159,9 +107,6 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       i = __shfl_sync(kFull, i, src);
       n = __shfl_sync(kFull, n, src);
       fgn = __shfl_sync(kFull, fgn, src);
-#if TSF_PACKED_STAGE
-      orig = src;
-#endif
     }
 #endif
     int incl = n;
@@ -180,49 +125,22 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       if (mine) {
         s_atom[wbase + excl - base] = i;
         s_cnt[wbase + excl - base] = n;
-#if TSF_PACKED_STAGE
-        s_fgn[wbase + excl - base] = fgn | (orig << 1);
-#else
         s_fgn[wbase + excl - base] = fgn;
-#endif
       }
       __syncwarp();
       const bool slot = lane < used;
       const int h = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // bit 0 is set
       const int ai = s_atom[wbase + h];
       const int ni = slot ? s_cnt[wbase + h] : 0;
-#if TSF_PACKED_STAGE
-      const int hf = s_fgn[wbase + h];
-      const bool foreign = FOREIGN && (hf & 1);
-      const int orow = wbase + (hf >> 1);
-#else
       const bool foreign = FOREIGN && s_fgn[wbase + h];
-#endif
       const int gl = lane - h;
       TSF_DCHECK(h >= 0 && h <= lane && ai >= 0 && ai <= last, "k_force_packed segment head");
       TSF_DCHECK(!slot || (gl < ni && ni <= 32), "k_force_packed segment slot");
-#if TSF_PACKED_STAGE
-      int v = ai;
-      if (slot) {
-        if (gl < 8) {
-          const int4 e = s_list[orow][gl >> 2];
-          const int c = gl & 3;
-          v = c == 0 ? e.x : c == 1 ? e.y : c == 2 ? e.z : e.w;
-        } else {
-          v = a.nbr[ell_at(gl, ai, a.npad)];
-        }
-      }
-      TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
-      const int j = unsigned(v) <= unsigned(last) ? v : ai;
-      const double4 pi = s_posi[orow];
-      const double4 pj = a.pos[j];
-#else
       const int v = slot ? a.nbr[ell_at(gl, ai, a.npad)] : ai;
       TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
       const int j = unsigned(v) <= unsigned(last) ? v : ai;
       const double4 pi = a.pos[ai];
       const double4 pj = a.pos[j];
-#endif
 
       double dx = 0, dy = 0, dz = 0, r2 = 1.0;
       if (slot) {
@@ -439,6 +357,97 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       }
       base += used;
       __syncwarp();                      // staging and heads are rewritten by the next pack
+    }
+  };
+
+  if constexpr (OVF) {
+    if (a.over4 && *a.over4 == 0) {        // the filter saw no count over 4
+      if (tid < kRedWidth)
+        a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
+      return;
+    }
+    // ---- tier launch behind a width-G main launch: the atoms it left are
+    // exactly the owned centres with more than scan_g short entries.  Each
+    // warp scans its own contiguous slot range (counts coalesced, 32 per
+    // step), compacts those atoms in slot order into a per-warp buffer and
+    // runs a chunk whenever 32 are waiting — no queue, no atomics (a queue
+    // fed by one counter serialised 180k same-address atomics in the main
+    // launch at 1600 K), and neighbouring atoms share their gathers ----
+    int* bi = s_buf[tid / 32];
+    int* bn = s_buf[tid / 32] + 64;
+    const int lo = a.slot_base, hi = a.n_owned;
+    const int per = ((hi - lo + nwarps - 1) / nwarps + 31) & ~31;
+    const int w0 = lo + warp * per, w1 = min(hi, w0 + per);
+    int nb = 0, s0 = w0;                         // warp-uniform
+    while (true) {
+      while (nb < 32 && s0 < w1) {               // fill the buffer to a chunk
+        const int sl = s0 + lane;
+        int c = sl < w1 ? a.cnt[sl] : 0;
+        if (c > a.scan_g && has_ghosts && (a.perm ? a.perm[sl] : sl) >= a.center_limit) c = 0;
+        const bool over = c > a.scan_g;
+        const unsigned m = __ballot_sync(kFull, over);
+        if (over) {
+          const int q = nb + __popc(m & ((1u << lane) - 1u));
+          bi[q] = sl;
+          bn[q] = c;
+        }
+        nb += __popc(m);
+        s0 += 32;
+      }
+      if (nb == 0) break;
+      __syncwarp();
+      const int take = min(nb, 32);
+      const bool in = lane < take;
+      const int i = in ? bi[lane] : 0;
+      int n = in ? bn[lane] : 0;
+      __syncwarp();
+      if (lane < nb - 32) {                      // keep the rest (at most 31)
+        bi[lane] = bi[32 + lane];
+        bn[lane] = bn[32 + lane];
+      }
+      nb -= take;
+      if (n > 32) {                              // no wider launch behind this one
+        atomicOr(a.flags, kErrShortOverflow);
+        n = 0;
+      }
+      const int fgn = has_foreign && in && (a.perm ? a.perm[i] : i) >= a.energy_limit;
+      chunk_body(i, n, fgn);
+    }
+  } else {
+    // the main launch: chunks of 32 consecutive slots
+    const int items = a.n_owned - a.slot_base;
+    constexpr int cw = 32;
+    const int chunks = (items + cw - 1) / cw;
+    for (int chunk = warp; chunk < chunks; chunk += nwarps) {
+      // ---- this lane's atom of the chunk and its count ----
+      const int q = chunk * cw + lane;
+      const bool in = lane < cw && q < items;
+      const int i = in ? a.slot_base + q : 0;
+      int n = in ? a.cnt[i] : 0;
+      if (!OVF && has_ghosts && in && (a.perm ? a.perm[i] : i) >= a.center_limit) {
+        // a decomposition ghost copy: receives forces, is not a centre
+        if (DET) {   // zero its self term and the slots k_gather reads
+          Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+          f[0] = f[1] = f[2] = Acc(0);
+          for (int sl = 0; sl < n; ++sl) {
+            const std::size_t qs = std::size_t(sl) * a.npad + i;
+            static_cast<Acc*>(a.slot_x)[qs] = Acc(0);
+            static_cast<Acc*>(a.slot_y)[qs] = Acc(0);
+            static_cast<Acc*>(a.slot_z)[qs] = Acc(0);
+          }
+        }
+        n = 0;
+      }
+      if (n > 32) {                        // no wider launch behind this one
+        atomicOr(a.flags, kErrShortOverflow);
+        n = 0;
+      }
+      if (DET && in && n == 0) {           // no segment, no head: F_self = 0 here
+        Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(i);
+        f[0] = f[1] = f[2] = Acc(0);
+      }
+      const int fgn = has_foreign && in && (a.perm ? a.perm[i] : i) >= a.energy_limit;
+      chunk_body(i, n, fgn);
     }
   }
 

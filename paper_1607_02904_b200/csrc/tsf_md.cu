@@ -142,8 +142,11 @@ struct Masses {
   double m[kMaxSpecies];
 };
 
+// (__grid_constant__: the species-indexed mass is read from the parameter
+// bank; a plain by-value struct indexed at run time is copied to local memory)
 __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
-                       int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n, Masses ms,
+                       int* __restrict__ cmax, double* __restrict__ vel, const double* __restrict__ f, int n,
+                       const __grid_constant__ Masses ms,
                        double dt, int drift, int kicks, Box box,
                        const double4* __restrict__ ref, double limit_sq,
                        int* __restrict__ moved_flag, const int* __restrict__ perm,
@@ -206,7 +209,8 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
 // fixed order then one block finishing the sum: deterministic.
 __global__ void __launch_bounds__(256) k_ke_partial(const double4* __restrict__ pos,
                                                     const double* __restrict__ vel, int n,
-                                                    Masses ms, double* __restrict__ part,
+                                                    const __grid_constant__ Masses ms,
+                                                    double* __restrict__ part,
                                                     const int* __restrict__ perm,
                                                     int center_limit) {
   __shared__ double s[256];

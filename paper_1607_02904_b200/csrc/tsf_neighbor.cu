@@ -528,7 +528,8 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     ListArgs a, PairBounds pb, int apply, const int* __restrict__ skin,
     const int* __restrict__ skin_cnt, int* __restrict__ out, int* __restrict__ out_cnt,
     int* __restrict__ max_count, int* __restrict__ hist, void* __restrict__ zero_f,
-    int zero_bytes, int slot_lo, int slot_hi, NearIn near, int* __restrict__ zero_flags) {
+    int zero_bytes, int slot_lo, int slot_hi, NearIn near, int* __restrict__ zero_flags,
+    int* __restrict__ over4) {
   __shared__ float slo[kMaxSpecies * kMaxSpecies], shi[kMaxSpecies * kMaxSpecies];
   __shared__ double sc2[kMaxSpecies * kMaxSpecies];
   // a speculative step whose list went stale (this step's kick, or an
@@ -590,6 +591,11 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
     w = m;
   }
   out_cnt[at] = w;
+  if (over4) {   // force path: does the packed tier behind G = 4 have work?
+    const unsigned act = __activemask();
+    if (__any_sync(act, w > 4) && (threadIdx.x & 31) == __ffs(act) - 1 && __ldcg(over4) == 0)
+      *over4 = 1;
+  }
   // largest count and occupancy histogram for the force kernel's group width,
   // after rebuilds only (same-address atomics from every warp are not free):
   // hist[0] = atoms with more than 4 short neighbours, hist[1] = more than 8
@@ -1000,7 +1006,10 @@ void list_filter(Ctx& c, FilterMode mode, void* zero_forces, int zero_bytes, int
         list_args(c), pb, mode != FilterMode::Copy ? 1 : 0, c.skin_list.nbr.get(),
         c.skin_list.cnt.get(), s.nbr.get(), s.cnt.get(), reread ? c.flags.get() + 4 : nullptr,
         c.flags.get() + 8, zero_forces, zero_forces ? zero_bytes : 0, lo, hi, near,
-        zero_flags ? c.flags.get() : nullptr);
+        zero_flags ? c.flags.get() : nullptr,
+        zero_flags && !c.main_packed ? c.flags.get() + kFlagOver4 : nullptr);
+    // (a packed main launch has no tier to gate: irregular systems skip the mark)
+    c.filter_marks_over4 = zero_flags && !c.main_packed;
     ++c.launches;
   }
   s.valid = true;
