@@ -131,17 +131,17 @@ template <> struct Stage<double> {
   double2 a[kBlock];   // ux, uy
   double2 b[kBlock];   // uz, r
   double2 c[kBlock];   // 1/r, fc
-  double2 d[kBlock];   // fc', meta (species, -1 when not a usable k)
+  double2 d[kBlock];   // fc', meta (species, -1 when not a usable k; int bits)
   __device__ void put(int t, const Nbr<double>& n, double fc, double dfc, int meta) {
     a[t] = make_double2(n.ux, n.uy);
     b[t] = make_double2(n.uz, n.r);
     c[t] = make_double2(n.ir, fc);
-    d[t] = make_double2(dfc, double(meta));
+    d[t] = make_double2(dfc, __hiloint2double(0, meta));
   }
-  __device__ void get(int t, Nbr<double>& n, double& fc, double& dfc, double& meta) const {
+  __device__ void get(int t, Nbr<double>& n, double& fc, double& dfc, int& meta) const {
     const double2 va = a[t], vb = b[t], vc = c[t], vd = d[t];
     n.ux = va.x; n.uy = va.y; n.uz = vb.x; n.r = vb.y; n.ir = vc.x;
-    fc = vc.y; dfc = vd.x; meta = vd.y;
+    fc = vc.y; dfc = vd.x; meta = __double2loint(vd.y);
   }
   __device__ void unit(int t, double& ux, double& uy, double& uz) const {
     const double2 va = a[t];
@@ -150,15 +150,15 @@ template <> struct Stage<double> {
 };
 template <> struct Stage<float> {
   float4 a[kBlock];    // ux, uy, uz, r
-  float4 b[kBlock];    // 1/r, fc, fc', meta
+  float4 b[kBlock];    // 1/r, fc, fc', meta (int bits)
   __device__ void put(int t, const Nbr<float>& n, float fc, float dfc, int meta) {
     a[t] = make_float4(n.ux, n.uy, n.uz, n.r);
-    b[t] = make_float4(n.ir, fc, dfc, float(meta));
+    b[t] = make_float4(n.ir, fc, dfc, __int_as_float(meta));
   }
-  __device__ void get(int t, Nbr<float>& n, float& fc, float& dfc, float& meta) const {
+  __device__ void get(int t, Nbr<float>& n, float& fc, float& dfc, int& meta) const {
     const float4 va = a[t], vb = b[t];
     n.ux = va.x; n.uy = va.y; n.uz = va.z; n.r = va.w; n.ir = vb.x;
-    fc = vb.y; dfc = vb.z; meta = vb.w;
+    fc = vb.y; dfc = vb.z; meta = __float_as_int(vb.w);
   }
   __device__ void unit(int t, float& ux, float& uy, float& uz) const {
     const float4 va = a[t];
@@ -196,9 +196,19 @@ __device__ __forceinline__ Grad<R> triplet(const Nbr<R>& j, const Nbr<R>& k, R f
   const R q2 = q * q;
   const R x = cubic ? p.tc * (q2 * q) : p.tc * q;
   R ex;
-  if constexpr (!std::is_same<R, double>::value) ex = Fn<R>::exp_row(x);   // base 2
-  else if constexpr (EXPNB) ex = Fn<R>::exp_nb(x);
-  else ex = TSF_EXP_FIN >= 1 ? Fn<R>::exp_fin(x) : Fn<R>::exp_(x);
+  if constexpr (!std::is_same<R, double>::value) {
+    ex = Fn<R>::exp_row(x);   // base 2
+  } else if constexpr (EXPNB) {
+    ex = Fn<R>::exp_nb(x);
+  } else if constexpr (CUB < 0) {
+    // multi-species tables: Tersoff's 1989 SiC / SiGe rows carry lambda3 = 0,
+    // where the factor is exactly e^0 = 1 (uniform branch; 11% of the SiC
+    // kernel's instructions were that exp)
+    if (p.tc != R(0)) ex = TSF_EXP_FIN >= 1 ? Fn<R>::exp_fin(x) : Fn<R>::exp_(x);
+    else ex = R(1);
+  } else {
+    ex = TSF_EXP_FIN >= 1 ? Fn<R>::exp_fin(x) : Fn<R>::exp_(x);
+  }
   const R gx = g * ex;
   o.z = fck * gx;
   const R fge = o.z * (cubic ? p.td * q2 : p.td);                      // dz/dr_ij via exp
@@ -469,12 +479,13 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       if (m >= n_i) m -= n_i;
       const int src = gbase + (m & (G - 1));
       Nbr<R> k;
-      R fck, dfck, kmeta;
+      R fck, dfck;
+      int kmeta;
       st.get(src, k, fck, dfck, kmeta);
-      bool ok = pair_ok && t < n_i && kmeta >= R(0);
+      bool ok = pair_ok && t < n_i && kmeta >= 0;
       const Row<R>* prow = &pjj;
       if (SPEC != kSingle) {
-        const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+        const int sk = max(kmeta, 0);
         prow = &srow[rowbase + sk];
         if (SPEC == kGeneric) {
           ok = ok && s_r2[src] <= scut[rowbase + sk];
@@ -534,12 +545,13 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         if (m >= n_i) m -= n_i;
         const int src = gbase + (m & (G - 1));
         Nbr<R> k;
-        R fck, dfck, kmeta;
+        R fck, dfck;
+        int kmeta;
         st.get(src, k, fck, dfck, kmeta);
-        bool ok = pair_ok && t < n_i && kmeta >= R(0);
+        bool ok = pair_ok && t < n_i && kmeta >= 0;
         const Row<R>* prow = &pjj;
         if (SPEC != kSingle) {
-          const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+          const int sk = max(kmeta, 0);
           prow = &srow[rowbase + sk];
           if (SPEC == kGeneric) {
             ok = ok && s_r2[src] <= scut[rowbase + sk];

@@ -178,12 +178,13 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
           if (m >= ni) m -= ni;
         }
         const int src = wbase + h + m;
-        R fck, dfck, kmeta;
+        R fck, dfck;
+        int kmeta;
         st.get(src, k, fck, dfck, kmeta);
-        bool ok = pair_ok && t < ni && kmeta >= R(0);
+        bool ok = pair_ok && t < ni && kmeta >= 0;
         const Row<R>* prow = &pjj;
         if (SPEC != kSingle) {
-          const int sk = kmeta >= R(0) ? int(kmeta) : 0;
+          const int sk = max(kmeta, 0);
           prow = &srow[rowbase + sk];
           if (SPEC == kGeneric) {
             ok = ok && s_r2[src] <= scut[rowbase + sk];

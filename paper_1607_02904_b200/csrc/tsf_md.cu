@@ -193,7 +193,8 @@ __global__ void k_kick(double4* __restrict__ pos, float4* __restrict__ posf,
       displacement(ref[a], p, box, dx, dy, dz);
       const double d2 = norm_sq_exact(dx, dy, dz);
       const unsigned act = __activemask();
-      if (moved_flag && __any_sync(act, d2 > limit_sq) && (threadIdx.x & 31) == __ffs(act) - 1) {
+      if (moved_flag && __any_sync(act, d2 > limit_sq) && (threadIdx.x & 31) == __ffs(act) - 1 &&
+          __ldcg(moved_flag) == 0) {   // (thousands of warps at a rebuild step: one address)
         atomicOr(moved_flag, 1);
         if (seg_flags) seg_flags[kFlagMovedStep] = seg_step;   // same value from every writer
       }

@@ -47,11 +47,14 @@ __device__ __forceinline__ int clamp_cell(double p, double org, double ext, int 
   return c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
 }
 
-// atomicMax from one lane per converged subset.
+// atomicMax from one lane per converged subset, only when it can raise the
+// value: one address takes every warp's update (64k per 2M-atom launch), and
+// same-address atomics serialise in L2 — once the maximum is reached a plain
+// cached read filters almost all of them out.
 __device__ __forceinline__ void warp_atomic_max(int* p, int v) {
   const unsigned act = __activemask();
   const int m = __reduce_max_sync(act, v);
-  if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(p, m);
+  if ((threadIdx.x & 31) == __ffs(act) - 1 && m > __ldcg(p)) atomicMax(p, m);
 }
 
 // Sort key (cell, user index) per slot; counts per cell; largest occupancy.
@@ -636,9 +639,26 @@ __global__ void k_extent(const double4* __restrict__ pos, int n,
   if (a >= n) return;
   const double4 p = pos[a];
   const double v[3] = {p.x, p.y, p.z};
+  // warp-reduced, then one lane per warp and only when it moves a bound (six
+  // same-address atomics per atom serialised in L2)
+  const unsigned act = __activemask();
+  const bool first = (threadIdx.x & 31) == __ffs(act) - 1;
+#pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
-    atomicMin(mnmx + ax, ordered_key(v[ax]));
-    atomicMax(mnmx + 3 + ax, ordered_key(v[ax]));
+    unsigned long long lo = ordered_key(v[ax]), hi = lo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(act, lo, o), h2 = __shfl_xor_sync(act, hi, o);
+      const bool ok = (act >> ((threadIdx.x & 31) ^ o)) & 1u;   // partner active
+      if (ok) {
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+      }
+    }
+    if (first) {
+      if (lo < __ldcg(mnmx + ax)) atomicMin(mnmx + ax, lo);
+      if (hi > __ldcg(mnmx + 3 + ax)) atomicMax(mnmx + 3 + ax, hi);
+    }
   }
 }
 
