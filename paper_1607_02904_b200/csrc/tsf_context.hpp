@@ -158,7 +158,7 @@ struct Ctx {
   DevBuf<double4> tmp4;        // re-sort scratch
   DevBuf<double> tmp3;
   DevBuf<int> tmp_i;
-  DevBuf<unsigned long long> sort_keys, sort_keys_out;
+  DevBuf<unsigned> sort_keys, sort_keys_out;   // cell ids, indexed by user atom
   DevBuf<int> sort_vals, sort_vals_out;
   double* pinned = nullptr;    // pinned host staging, pinned_cap doubles
   std::size_t pinned_cap = 0;
