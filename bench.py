@@ -289,7 +289,8 @@ def workload_config(args, n, world, halo, parallelism):
     return {
         "workload": CONFIGS[args.config][4] + (f", seeded uniform +-{jit:.2f} A jitter" if jit
                                                else "") +
-                    ", skin 1.0 A; one filter + force/energy/virial evaluation per step",
+                    ", skin 1.0 A; one filter + force/energy" +
+                    ("" if getattr(args, "no_virial", False) else "/virial") + " evaluation per step",
         "n_atoms": n, "precision": args.precision,
         "deterministic": bool(args.deterministic),
         "parallelism": parallelism or (f"{world} x-slab domains" if world > 1 else "single GPU"),
