@@ -273,9 +273,17 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       // ---- F_i = -sum of the segment's P (and, queued + deterministic, the
       // atom's energy and virial), summed by the head lane in slot order ----
       const R rx = R(dx), ry = R(dy), rz = R(dz);
-      s_seg[0][tid] = Acc(px);
-      s_seg[1][tid] = Acc(py);
-      s_seg[2][tid] = Acc(pz);
+      // FP64 atomic mode: each slot lane adds -P to F_i itself (three more
+      // reductions per slot instead of the head lane's serial segment sum,
+      // which ran max(n_i) iterations with one lane in 32 active: -5% on the
+      // f64 SiC and liquid kernels; the float kernels measured +1%, so they
+      // keep the sum); deterministic mode sums in slot order
+      constexpr bool kLaneAtomics = !DET && std::is_same<R, double>::value;
+      if (!kLaneAtomics) {
+        s_seg[0][tid] = Acc(px);
+        s_seg[1][tid] = Acc(py);
+        s_seg[2][tid] = Acc(pz);
+      }
       if constexpr (OVF && DET) {
         const bool cnt_ev = slot && !(FOREIGN && foreign);
         s_seg[3][tid] = cnt_ev ? Acc(vv) : Acc(0);
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       Acc evsum[7] = {0, 0, 0, 0, 0, 0, 0};
       const bool head = slot && gl == 0;
       TSF_DCHECK(!head || lane + ni <= 32, "k_force_packed segment sum");
-      if (head) {
+      if (!kLaneAtomics && head) {
         for (int u = 0; u < ni; ++u) {
           fsum[0] += s_seg[0][tid + u];
           fsum[1] += s_seg[1][tid + u];
@@ -341,9 +349,15 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
           atomicAdd(f + 0, Acc(px));
           atomicAdd(f + 1, Acc(py));
           atomicAdd(f + 2, Acc(pz));
+          if constexpr (kLaneAtomics) {
+            Acc* fi = static_cast<Acc*>(a.forces) + 3 * std::size_t(ai);
+            atomicAdd(fi + 0, -Acc(px));
+            atomicAdd(fi + 1, -Acc(py));
+            atomicAdd(fi + 2, -Acc(pz));
+          }
         }
       }
-      if (head) {
+      if (!kLaneAtomics && head) {
         if (DET) {
           Acc* f = static_cast<Acc*>(a.fself) + 3 * std::size_t(ai);
           f[0] = -fsum[0];

@@ -24,6 +24,22 @@ __global__ void fma_kernel(T* out, T a, T b) {
   if (s == T(-1.2345)) out[0] = s;
 }
 
+// packed FP32 (sm_100: FFMA2, one instruction for two lanes' worth of FMAs)
+__global__ void fma2_kernel(float* out, float a, float b) {
+  float2 acc[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) acc[c] = make_float2(threadIdx.x + c, threadIdx.x - c);
+  const float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c] = __ffma2_rn(acc[c], a2, b2);
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += acc[c].x + acc[c].y;
+  if (s == -1.2345f) out[0] = s;
+}
+
 __global__ void mufu_kernel(float* out, float a) {
   float acc[kChains];
 #pragma unroll
@@ -71,16 +87,19 @@ int main() {
   const double t64 = time_ms([&] { fma_kernel<double><<<blocks, threads>>>(d64, 0.999, 1e-3); });
   const double t32 = time_ms([&] { fma_kernel<float><<<blocks, threads>>>(d32, 0.999f, 1e-3f); });
   const double tmu = time_ms([&] { mufu_kernel<<<blocks, threads>>>(d32, 0.5f); });
+  const double tf2 = time_ms([&] { fma2_kernel<<<blocks, threads>>>(d32, 0.999f, 1e-3f); });
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   std::printf(
       "{\"gpu\": \"%s\", \"sms\": %d, \"clock_mhz_attr\": %.0f, "
-      "\"fp64_tflops\": %.3f, \"fp32_tflops\": %.3f, \"mufu_ex2_gops\": %.1f, "
+      "\"fp64_tflops\": %.3f, \"fp32_tflops\": %.3f, \"fp32x2_tflops\": %.3f, "
+      "\"mufu_ex2_gops\": %.1f, "
       "\"fp64_fma_per_clk_sm\": %.1f, \"fp32_fma_per_clk_sm\": %.1f, "
       "\"how\": \"8 independent FMA chains x 4096 iters, %d blocks x %d threads, best of 5; "
       "TFLOP/s counts an FMA as 2 flops\"}\n",
       prop.name, sms, clk / 1e3, 2.0 * lanes / (t64 * 1e-3) / 1e12,
-      2.0 * lanes / (t32 * 1e-3) / 1e12, lanes / (tmu * 1e-3) / 1e9,
+      2.0 * lanes / (t32 * 1e-3) / 1e12, 4.0 * lanes / (tf2 * 1e-3) / 1e12,
+      lanes / (tmu * 1e-3) / 1e9,
       lanes / (t64 * 1e-3) / sms / (clk * 1e3), lanes / (t32 * 1e-3) / sms / (clk * 1e3), blocks,
       threads);
   return 0;

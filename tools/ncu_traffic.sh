@@ -22,7 +22,7 @@ for C in $CFGS; do
     M=$M,sm__throughput.avg.pct_of_peak_sustained_elapsed
     ncu --metrics $M \
         --clock-control none --kernel-name-base demangled --nvtx --nvtx-include "bench_steps/" \
-        -k 'regex:k_force(_packed)?<.*\(bool\)0, \(bool\)0>|k_filter' -s 2 -c 4 --csv \
+        -k 'regex:k_force<[^(]*\(int\)[0-9]+, \(int\)[0-9]+, \(bool\)[01], \(bool\)0|k_force_packed<[^(]*\(int\)[0-9]+, \(bool\)[01], \(bool\)0|k_filter' -s 2 -c 4 --csv \
         --log-file gpurun_out/traffic/${C}_$P.csv $B > gpurun_out/traffic/ncu_${C}_$P.log 2>&1
     echo "ncu $C $P rc=$?"
   done
