@@ -156,7 +156,8 @@ int tsf_evaluate_forces(tsf_ctx* ctx, int precision, int64_t n, const double* xy
  * libdevice log (out[2q] = f(x[q])); 4 bond order b, db/dzeta at zeta = x[q]
  * in double, 5 in float, 6 the reference's pow form in double (row (0,0,0)
  * of p; out[2q] = b, out[2q+1] = db); 7 the double bond order's path at
- * zeta = x[q] (out[2q] = 1 for the series, out[2q+1] = ln u). */
+ * zeta = x[q] (out[2q] = 1 for the series, out[2q+1] = ln u); 8 the cutoff
+ * ramp's sin(pi x), cos(pi x) for |x| <= 1/2, 9 libdevice sincospi. */
 int tsf_math_probe(const tsf_params* p, int fn, int64_t n, const double* x, double* out);
 
 /* Kernel launches issued by this context since creation (evidence counter). */

@@ -60,6 +60,8 @@ __global__ void k_math_probe(int fn, int n, const double* __restrict__ x, Row<do
       b = dbf;
       break;
     }
+    case 8: Fn<double>::sincospi_(v, &a, &b); break;   // the cutoff ramp's (|x| <= 1/2)
+    case 9: sincospi(v, &a, &b); break;
     case 7: {    // which path the double bond order takes: a = 1 series, b = ln u
       const double xb = rd.beta * v;
       b = rd.eta * log_cb(xb);
@@ -83,7 +85,7 @@ __global__ void k_math_probe(int fn, int n, const double* __restrict__ x, Row<do
 }  // namespace
 
 void math_probe(const Params& p, int fn, std::int64_t n, const double* x, double* out) {
-  if (fn < 0 || fn > 7) throw ConfigError("unknown probe function");
+  if (fn < 0 || fn > 9) throw ConfigError("unknown probe function");
   if (n <= 0) return;
   double *dx = nullptr, *dy = nullptr;
   TSF_CUDA(cudaMalloc(&dx, sizeof(double) * n));

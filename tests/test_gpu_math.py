@@ -72,3 +72,16 @@ def test_bond_order_paths(tb, si, sic_text, table):
         assert (taken == 1.0).all(), lnu
     else:   # only for tiny zeta (u < 2^-12)
         assert list(taken) == [1.0, 1.0, 0.0, 0.0, 0.0] and lnu[2] > 0, lnu
+
+
+def test_ramp_sincospi_against_libdevice(tb, si):
+    """The cutoff ramp's branch-free sin(pi x), cos(pi x) (|x| <= 1/2, the
+    whole ramp R - D < r < R + D; potential.hpp:58-69) against libdevice's
+    sincospi: within 2.5e-16 absolute, exact at the ramp's centre."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-0.5, 0.5, 40000), [-0.5, -0.25, 0.0, 0.25, 0.5]])
+    s, c = probe(tb, si, 8, x)
+    rs, rc = probe(tb, si, 9, x)
+    assert np.abs(s - rs).max() <= 2.5e-16 and np.abs(c - rc).max() <= 2.5e-16
+    s0, c0 = probe(tb, si, 8, [0.0])
+    assert s0[0] == 0.0 and c0[0] == 1.0
