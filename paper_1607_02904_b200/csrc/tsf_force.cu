@@ -60,7 +60,7 @@ __global__ void k_math_probe(int fn, int n, const double* __restrict__ x, Row<do
       b = dbf;
       break;
     }
-    case 8: Fn<double>::sincospi_(v, &a, &b); break;   // the cutoff ramp's (|x| <= 1/2)
+    case 8: Fn<double>::sincospi_half(v, &a, &b); break;   // the cutoff ramp's (|x| <= 1/2)
     case 9: sincospi(v, &a, &b); break;
     case 7: {    // which path the double bond order takes: a = 1 series, b = ln u
       const double xb = rd.beta * v;

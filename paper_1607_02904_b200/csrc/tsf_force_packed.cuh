@@ -21,14 +21,14 @@
 namespace tsf {
 namespace {
 
-#ifndef TSF_PACKED_SORT
-#define TSF_PACKED_SORT 1
-#endif
 #ifndef TSF_PACKED_CACHE_F64
 #define TSF_PACKED_CACHE_F64 5
 #endif
 #ifndef TSF_PACKED_CACHE_F32
 #define TSF_PACKED_CACHE_F32 7
+#endif
+#ifndef TSF_PACKED_AHEAD
+#define TSF_PACKED_AHEAD 1
 #endif
 template <typename R>
 constexpr int kPackedCacheRot =
@@ -48,15 +48,15 @@ template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN =
 __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
     k_force_packed(const __grid_constant__ ForceArgs<R> a) {
   constexpr int kC = kPackedCacheRot<R>;
+  // next-pack lookahead (below): float liquid -4%, single -5%; the FP64
+  // kernels spill with it (SiC f64 +4%) and keep the plain order
+  constexpr bool kAhead = TSF_PACKED_AHEAD && !std::is_same<R, double>::value;
   constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
   __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
   __shared__ double scut[SPEC == kSingle ? 1 : kRows];
   __shared__ Stage<R> st;
   __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
   __shared__ double s_red[kBlock / 32][kRedWidth];
-  __shared__ int s_atom[kBlock];       // per segment head: slot, count, foreign
-  __shared__ int s_cnt[kBlock];
-  __shared__ int s_fgn[kBlock];
   __shared__ Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
   __shared__ int s_buf[OVF ? kBlock / 32 : 1][128];   // scanning tier: slots, counts
 
@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   // One chunk: this lane's atom i (slot) with short count n (0: none) and its
   // ghost-centre bit; the warp sorts, scans and packs the chunk's slots.
   auto chunk_body = [&](int i, int n, int fgn) {
-#if TSF_PACKED_SORT
     {
       // order the chunk's atoms by count (bitonic, key (n, lane): unique, so
       // deterministic): a pack then holds atoms of similar counts, and its
@@ -108,7 +107,6 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       n = __shfl_sync(kFull, n, src);
       fgn = __shfl_sync(kFull, fgn, src);
     }
-#endif
     int incl = n;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -118,29 +116,56 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
     const int excl = incl - n;
     const int total = __shfl_sync(kFull, incl, 31);
 
-    for (int base = 0; base < total;) {           // warp-uniform: one pack per pass
+    // Pack p's lane map without shared memory: the chunk is sorted by count,
+    // so its zero-count atoms come first and pack p's atoms are the next
+    // popc(heads) in sorted order; lane L's atom is the one whose segment
+    // head is the highest head bit at or below L.  The next pack's map and
+    // list entry are formed while this pack computes, its positions requested
+    // after the zeta pass (one dependent load chain per pack was the packed
+    // kernels' long-scoreboard stall).
+    struct PackLane {
+      int used, kb_next, h, gl, ai, ni, v;
+      bool slot, foreign;
+    };
+    auto pack_at = [&](int base, int kb, PackLane& P) {
       const bool mine = n > 0 && excl >= base && incl <= base + 32;
       const unsigned heads = __reduce_or_sync(kFull, mine ? 1u << (excl - base) : 0u);
-      const int used = int(__reduce_max_sync(kFull, mine ? unsigned(incl - base) : 0u));
-      if (mine) {
-        s_atom[wbase + excl - base] = i;
-        s_cnt[wbase + excl - base] = n;
-        s_fgn[wbase + excl - base] = fgn;
-      }
-      __syncwarp();
-      const bool slot = lane < used;
-      const int h = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // bit 0 is set
-      const int ai = s_atom[wbase + h];
-      const int ni = slot ? s_cnt[wbase + h] : 0;
-      const bool foreign = FOREIGN && s_fgn[wbase + h];
-      const int gl = lane - h;
-      TSF_DCHECK(h >= 0 && h <= lane && ai >= 0 && ai <= last, "k_force_packed segment head");
-      TSF_DCHECK(!slot || (gl < ni && ni <= 32), "k_force_packed segment slot");
-      const int v = slot ? a.nbr[ell_at(gl, ai, a.npad)] : ai;
+      P.used = int(__reduce_max_sync(kFull, mine ? unsigned(incl - base) : 0u));
+      const unsigned le = heads & (0xffffffffu >> (31 - lane));   // bit 0 is set
+      P.h = 31 - __clz(le);
+      const int k = (kb + __popc(le) - 1) & 31;
+      P.kb_next = kb + __popc(heads);
+      P.slot = lane < P.used;
+      P.ai = __shfl_sync(kFull, i, k);
+      const int nk = __shfl_sync(kFull, n, k);
+      P.foreign = FOREIGN && __shfl_sync(kFull, fgn, k);
+      P.ni = P.slot ? nk : 0;
+      P.gl = lane - P.h;
+      TSF_DCHECK(P.h >= 0 && P.h <= lane && P.ai >= 0 && P.ai <= last, "k_force_packed segment head");
+      TSF_DCHECK(!P.slot || (P.gl < P.ni && P.ni <= 32), "k_force_packed segment slot");
+      P.v = P.slot ? a.nbr[ell_at(P.gl, P.ai, a.npad)] : P.ai;
+    };
+    PackLane cur;
+    pack_at(0, __popc(__ballot_sync(kFull, n == 0)), cur);
+    double4 pi_c, pj_c;
+    {
+      const int j0 = unsigned(cur.v) <= unsigned(last) ? cur.v : cur.ai;
+      pi_c = a.pos[cur.ai];
+      pj_c = a.pos[j0];
+    }
+    for (int base = 0; base < total;) {           // warp-uniform: one pack per pass
+      const bool slot = cur.slot;
+      const int ai = cur.ai, ni = cur.ni, h = cur.h, gl = cur.gl, used = cur.used;
+      const bool foreign = cur.foreign;
+      const int v = cur.v;
       TSF_DCHECK(!slot || (v >= 0 && v <= last && v != ai), "k_force_packed list entry");
       const int j = unsigned(v) <= unsigned(last) ? v : ai;
-      const double4 pi = a.pos[ai];
-      const double4 pj = a.pos[j];
+      const double4 pi = pi_c;
+      const double4 pj = pj_c;
+      // the next pack: lane map and list entry now, positions after the zeta pass
+      const bool more = base + used < total;   // warp-uniform
+      PackLane nxt = cur;
+      if (kAhead && more) pack_at(base + used, cur.kb_next, nxt);
 
       double dx = 0, dy = 0, dz = 0, r2 = 1.0;
       if (slot) {
@@ -159,7 +184,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       me.uy = R(dy) * me.ir;
       me.uz = R(dz) * me.ir;
       R fc, dfc;
-      cutoff_ramp(me.r, pjj, fc, dfc);
+      cutoff_ramp<R, true>(me.r, pjj, fc, dfc);
       const R fr = pjj.a * Fn<R>::exp_row(pjj.e1 * me.r);
       const R fa = -(pjj.b * Fn<R>::exp_row(pjj.e2 * me.r));
       const int meta = SPEC == kGeneric ? (slot ? sj : -1) : (pair_ok ? sj : -1);
@@ -188,7 +213,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
           prow = &srow[rowbase + sk];
           if (SPEC == kGeneric) {
             ok = ok && s_r2[src] <= scut[rowbase + sk];
-            cutoff_ramp(k.r, *prow, fck, dfck);
+            cutoff_ramp<R, true>(k.r, *prow, fck, dfck);
           }
         }
         fck = ok ? fck : R(0);
@@ -221,6 +246,12 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       for (int t = kC + 1; t < tmax; ++t) {
         Nbr<R> k;
         accumulate(triplet_at(t, k), k);
+      }
+
+      if (kAhead && more) {
+        const int jn = unsigned(nxt.v) <= unsigned(last) ? nxt.v : nxt.ai;
+        pi_c = a.pos[nxt.ai];
+        pj_c = a.pos[jn];
       }
 
       // ---- pair block ----
@@ -370,8 +401,15 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
           atomicAdd(f + 2, -fsum[2]);
         }
       }
+      if (!kAhead && more) {
+        pack_at(base + used, cur.kb_next, nxt);
+        const int jn = unsigned(nxt.v) <= unsigned(last) ? nxt.v : nxt.ai;
+        pi_c = a.pos[nxt.ai];
+        pj_c = a.pos[jn];
+      }
       base += used;
-      __syncwarp();                      // staging and heads are rewritten by the next pack
+      cur = nxt;
+      __syncwarp();                      // staging is rewritten by the next pack
     }
   };
 
