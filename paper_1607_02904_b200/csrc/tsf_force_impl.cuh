@@ -92,6 +92,11 @@ struct ForceArgs {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// non-blocking L2 prefetch (no register is written)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Which exponentials use the branch-free constant-bank exp (tsf_math.cuh
 // exp_cb, Estrin) instead of libdevice's: 0 none, 1 the triplet's, 2 also the
 // pair terms'.  Measured (tools/ab.py, si2m f64 kernel): 0 0.320 ms, 1 0.344,

@@ -89,6 +89,18 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   // One chunk: this lane's atom i (slot) with short count n (0: none) and its
   // ghost-centre bit; the warp sorts, scans and packs the chunk's slots.
   auto chunk_body = [&](int i, int n, int fgn) {
+    if constexpr (OVF) {
+      // the chunk's neighbour positions, one lane per atom, before the packs
+      // walk them serially
+      if (n > 0) {
+        const int4 e = *reinterpret_cast<const int4*>(a.nbr + ell_at(0, i, a.npad));
+        prefetch_l2(&a.pos[min(max(e.x, 0), last)]);
+        prefetch_l2(&a.pos[min(max(e.y, 0), last)]);
+        prefetch_l2(&a.pos[min(max(e.z, 0), last)]);
+        prefetch_l2(&a.pos[min(max(e.w, 0), last)]);
+        for (int q = 4; q < n; ++q) prefetch_l2(&a.pos[min(max(a.nbr[ell_at(q, i, a.npad)], 0), last)]);
+      }
+    }
     {
       // order the chunk's atoms by count (bitonic, key (n, lane): unique, so
       // deterministic): a pack then holds atoms of similar counts, and its
@@ -443,6 +455,12 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
           const int q = nb + __popc(m & ((1u << lane) - 1u));
           bi[q] = sl;
           bn[q] = c;
+          // into L2 while the chunk fills: the atom's position and list
+          // blocks (the tier's atoms are sparse: its loads missed L1 81%
+          // and L2 57% of the time, long-scoreboard stalls 3.5 per issue)
+          prefetch_l2(&a.pos[sl]);
+          prefetch_l2(a.nbr + ell_at(0, sl, a.npad));
+          if (c > 4) prefetch_l2(a.nbr + ell_at(4, sl, a.npad));
         }
         nb += __popc(m);
         s0 += 32;
