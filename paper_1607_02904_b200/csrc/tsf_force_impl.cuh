@@ -256,8 +256,29 @@ constexpr int kForceMinBlocks = G == 8 ? TSF_FORCE_MINB_F64_G8 : TSF_FORCE_MINB_
 template <int G>
 constexpr int kForceMinBlocks<float, G> = G == 8 ? TSF_FORCE_MINB_F32_G8 : TSF_FORCE_MINB_F32;
 
+}  // namespace
+}  // namespace tsf
+#include "tsf_force_packed.cuh"
+namespace tsf {
+namespace {
+
+#ifndef TSF_MERGE_TIER
+#define TSF_MERGE_TIER 1
+#endif
+// MERGE: the FP64 single-species G = 4 main launch runs the packed tier
+// itself (packed_work, OVF) after its tiles — the atoms over 4 found by the
+// same count scan — so the separate tier launch leaves the chain (both use
+// 128 registers; the float main kernel's 80 would not survive the merge).
+// Small systems only (kMergeMaxAtoms): at 32k atoms the evaluation is a chain
+// of latency-bound launches (-11% per evaluation, -7% per MD step), while at
+// 2M the merged code's spills in the main loop cost more than the launch.
+constexpr std::int64_t kMergeMaxAtoms = 1 << 20;
+template <typename R, int G, int SPEC, bool OVF>
+constexpr bool kMergeTier =
+    TSF_MERGE_TIER && G == 4 && SPEC == kSingle && !OVF && std::is_same<R, double>::value;
+
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
-          bool VIR = true, bool EXPNB = false>
+          bool VIR = true, bool EXPNB = false, bool MERGE = false>
 __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     k_force(const __grid_constant__ ForceArgs<R> a) {
 #ifndef TSF_CACHE_G16
@@ -277,6 +298,8 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
   __shared__ Stage<R> st;
   __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
   __shared__ double s_red[kBlock / 32][kRedWidth];
+  constexpr bool kMerge = MERGE && kMergeTier<R, G, SPEC, OVF>;
+  __shared__ std::conditional_t<kMerge, PackedShared<R, Acc, SPEC, DET, true>, char> s_tier;
 
   griddep_wait();     // launch_pdl: the previous launch has completed
   griddep_launch();
@@ -653,6 +676,11 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     __syncwarp();                      // staging is rewritten by the next tile
   }
 
+  if constexpr (kMerge) {
+    // the atoms over 4 (left above), by the packed tier's own scan
+    if (a.ovf_scan) packed_work<R, Acc, SPEC, DET, true, FOREIGN, VIR>(a, s_tier, e_acc, w_acc);
+  }
+
   // ---- block reduction of energy + virial, fixed order ----
   double red[7] = {double(e_acc), double(w_acc[0]), double(w_acc[1]), double(w_acc[2]),
                    double(w_acc[3]), double(w_acc[4]), double(w_acc[5])};
@@ -671,12 +699,6 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = s;
   }
 }
-
-}  // namespace
-}  // namespace tsf
-#include "tsf_force_packed.cuh"
-namespace tsf {
-namespace {
 
 // Sum of the block partials in a fixed order.  The partials are read as one
 // flat array: thread t always holds quantity q = t % 8 (1024 % kRedWidth == 0),
@@ -864,16 +886,19 @@ int persistent_blocks(K kernel, int tiles) {
 constexpr int kOverflowBlocks = 4 * 148;   // per tier launch; idle tiers exit at once
 
 template <typename R, typename Acc, int G, int SPEC, bool DET, bool FOREIGN, bool VIR = true>
-int launch_main(Ctx& c, ForceArgs<R> a) {
+int launch_main(Ctx& c, ForceArgs<R> a, bool merge = false) {
   const int tiles = std::max(1, ceil_div(a.n_owned - a.slot_base, kBlock / G));
   auto kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR>;
+  if constexpr (kMergeTier<R, G, SPEC, false>)
+    if (merge) kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR, false, true>;
   // one species, FP64, G = 4: the branch-free exp when the row bounds every
   // argument (Si: (lambda3 R)^3 = 76) — TSF_EXPNB=1 turns it on
   if constexpr (SPEC == kSingle && G == 4 && std::is_same<R, double>::value) {
     // measured slower (+6% on si2m: the interleaved chains spill): A/B only
     const char* e = std::getenv("TSF_EXPNB");
     if (a.row0.exp_ok != R(0) && e && e[0] == '1')
-      kern = k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR, true>;
+      kern = merge ? k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR, true, true>
+                   : k_force<R, Acc, G, SPEC, DET, false, FOREIGN, VIR, true>;
   }
   const int blocks = persistent_blocks(kern, tiles);
   c.mark(2);
@@ -959,6 +984,9 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
   a.ovf_out_count = a.flags + 1;
   // packed tier (default): the main launch queues nothing, the tier scans
   a.ovf_scan = pmode >= 1 && g < 32 ? 1 : 0;
+  const char* merge_env = std::getenv("TSF_MERGE_TIER");   // =0: separate tier launch (A/B)
+  const bool merge_tier = kMergeTier<R, 4, SPEC, false> && g == 4 && a.ovf_scan &&
+                          c.n <= kMergeMaxAtoms && !(merge_env && merge_env[0] == '0');
   a.scan_g = g;
   a.over4 = c.filter_marks_over4 && c.phase_first ? a.flags + kFlagOver4 : nullptr;
   // two-phase evaluation: the partials of the first phase's main launch
@@ -970,7 +998,7 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     nb += launch_main_packed<R, Acc, SPEC, DET, FOREIGN, VIR>(c, a);
   } else {
     switch (g) {
-      case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN, VIR>(c, a); break;
+      case 4: nb += launch_main<R, Acc, 4, SPEC, DET, FOREIGN, VIR>(c, a, merge_tier); break;
       case 8: nb += launch_main<R, Acc, 8, SPEC, DET, FOREIGN>(c, a); break;
       case 16: nb += launch_main<R, Acc, 16, SPEC, DET, FOREIGN>(c, a); break;
       default: nb += launch_main<R, Acc, 32, SPEC, DET, FOREIGN>(c, a); break;
@@ -996,7 +1024,10 @@ void run_force_t(Ctx& c, ForceArgs<R> a) {
     // rebuilds (Si at 1600 K: 0 -> 180k atoms with a 5th neighbour within 60
     // fs of a rebuild), and a quarter grid left 4 warps per SM to serialise
     // it (0.2 ms); an empty queue exits at once either way
-    if (g < 32) {
+    // (merged into the FP64 G = 4 main launches: each phase's main launch
+    // takes the atoms over 4 of its own slot range)
+    const bool merged = merge_tier;
+    if (g < 32 && !merged) {
       a.slot_base = 0;                      // every phase's slots
       tier(k_force_packed<R, Acc, SPEC, DET, true, FOREIGN, VIR>, kOverflowBlocks, true);
     }

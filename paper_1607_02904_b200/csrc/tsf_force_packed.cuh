@@ -43,31 +43,39 @@ template <typename R>
 constexpr int kPackedMinBlocks =
     std::is_same<R, double>::value ? TSF_PACKED_MINB_F64 : TSF_PACKED_MINB_F32;
 
-template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
-          bool VIR = true>
-__global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
-    k_force_packed(const __grid_constant__ ForceArgs<R> a) {
+// The packed kernel's shared memory (also embedded in k_force when the tier
+// is merged into the G = 4 main launch).
+template <typename R, typename Acc, int SPEC, bool DET, bool OVF>
+struct PackedShared {
+  static constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
+  Row<R> srow[SPEC == kSingle ? 1 : kRows];
+  double scut[SPEC == kSingle ? 1 : kRows];
+  Stage<R> st;
+  double s_r2[SPEC == kGeneric ? kBlock : 1];
+  Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
+  int s_buf[OVF ? kBlock / 32 : 1][128];     // scanning tier: slots, counts
+};
+
+// The packed lane groups' work of one block (main: chunks of consecutive
+// slots; OVF: the atoms over the main width, found by scanning the counts),
+// accumulating energy and virial into e_acc / w_acc.
+template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN, bool VIR>
+__device__ __forceinline__ void packed_work(const ForceArgs<R>& a,
+                                            PackedShared<R, Acc, SPEC, DET, OVF>& sh, Acc& e_acc,
+                                            Acc (&w_acc)[6]) {
   constexpr int kC = kPackedCacheRot<R>;
   // next-pack lookahead (below): float liquid -4%, single -5%; the FP64
   // kernels spill with it (SiC f64 +4%) and keep the plain order
   constexpr bool kAhead = TSF_PACKED_AHEAD && !std::is_same<R, double>::value;
-  constexpr int kRows = kMaxSpecies * kMaxSpecies * kMaxSpecies;
-  __shared__ Row<R> srow[SPEC == kSingle ? 1 : kRows];
-  __shared__ double scut[SPEC == kSingle ? 1 : kRows];
-  __shared__ Stage<R> st;
-  __shared__ double s_r2[SPEC == kGeneric ? kBlock : 1];
-  __shared__ double s_red[kBlock / 32][kRedWidth];
-  __shared__ Acc s_seg[(OVF && DET) ? 7 : 3][kBlock];   // segmented sums
-  __shared__ int s_buf[OVF ? kBlock / 32 : 1][128];   // scanning tier: slots, counts
-
-  griddep_wait();
-  griddep_launch();
-  if (a.skip && (a.skip[0] | a.skip[kFlagMovedAny - kFlagMoved])) return;   // stale list
+  auto& srow = sh.srow;
+  auto& scut = sh.scut;
+  auto& st = sh.st;
+  auto& s_r2 = sh.s_r2;
+  auto& s_seg = sh.s_seg;
+  auto& s_buf = sh.s_buf;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int wbase = tid - lane;
-  Acc e_acc = 0;
-  Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
 
   const int ns = a.ns;
   const Row<R>* rows = static_cast<const Row<R>*>(a.rows);
@@ -426,11 +434,7 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
   };
 
   if constexpr (OVF) {
-    if (a.over4 && *a.over4 == 0) {        // the filter saw no count over 4
-      if (tid < kRedWidth)
-        a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
-      return;
-    }
+    if (a.over4 && *a.over4 == 0) return;  // the filter saw no count over 4
     // ---- tier launch behind a width-G main launch: the atoms it left are
     // exactly the owned centres with more than scan_g short entries.  Each
     // warp scans its own contiguous slot range (counts coalesced, 32 per
@@ -521,6 +525,28 @@ __global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
       chunk_body(i, n, fgn);
     }
   }
+}
+
+template <typename R, typename Acc, int SPEC, bool DET, bool OVF, bool FOREIGN = false,
+          bool VIR = true>
+__global__ void __launch_bounds__(kBlock, kPackedMinBlocks<R>)
+    k_force_packed(const __grid_constant__ ForceArgs<R> a) {
+  __shared__ PackedShared<R, Acc, SPEC, DET, OVF> sh;
+  __shared__ double s_red[kBlock / 32][kRedWidth];
+
+  griddep_wait();
+  griddep_launch();
+  if (a.skip && (a.skip[0] | a.skip[kFlagMovedAny - kFlagMoved])) return;   // stale list
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (OVF && a.over4 && *a.over4 == 0) {   // the filter saw no count over 4
+    if (tid < kRedWidth)
+      a.partials[std::size_t(a.partial_base + blockIdx.x) * kRedWidth + tid] = 0.0;
+    return;
+  }
+  Acc e_acc = 0;
+  Acc w_acc[6] = {0, 0, 0, 0, 0, 0};
+  packed_work<R, Acc, SPEC, DET, OVF, FOREIGN, VIR>(a, sh, e_acc, w_acc);
 
   // ---- block reduction of energy + virial, fixed order ----
   double red[7] = {double(e_acc), double(w_acc[0]), double(w_acc[1]), double(w_acc[2]),
