@@ -338,6 +338,21 @@ bool graphs_enabled() {
   return on;
 }
 
+// A fresh capture goes into the slot's executable graph by cudaGraphExecUpdate
+// when the topology is unchanged (after a list rebuild: the same launches with
+// new parameters), else by a new instantiation — updates cost a fraction of an
+// instantiation, and an MD run re-captures after every rebuild.
+bool install_graph(cudaGraphExec_t& exec, cudaGraph_t g) {
+  if (exec) {
+    cudaGraphExecUpdateResultInfo info{};
+    if (cudaGraphExecUpdate(exec, g, &info) == cudaSuccess) return true;
+    cudaGetLastError();
+    cudaGraphExecDestroy(exec);
+    exec = nullptr;
+  }
+  return cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+}
+
 // Replay slot `slot`'s graph while its key holds; capture it on the second
 // eager run with the same key; else run eagerly.  `launches` must leave the
 // same host state on every run with one key (restored on replay).
@@ -355,10 +370,6 @@ void run_graphed(Ctx& c, int slot, bool graphable, const std::uint64_t* key, F&&
     std::copy(key, key + 6, s.warm);
     return;
   }
-  if (s.exec) {
-    TSF_CUDA(cudaGraphExecDestroy(s.exec));
-    s.exec = nullptr;
-  }
   const std::int64_t l0 = c.launches;
   const int pb0 = c.phase_blocks;
   cudaGraph_t g = nullptr;
@@ -370,7 +381,7 @@ void run_graphed(Ctx& c, int slot, bool graphable, const std::uint64_t* key, F&&
       ok = false;
     }
     ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
-    ok = ok && cudaGraphInstantiate(&s.exec, g, 0) == cudaSuccess;
+    ok = ok && install_graph(s.exec, g);
     if (g) cudaGraphDestroy(g);
   }
   if (ok) {
@@ -507,10 +518,6 @@ void run_segment(Ctx& c, const std::uint64_t* key, bool graphable, F&& launches)
     launches();
     return;
   }
-  if (s.exec) {
-    TSF_CUDA(cudaGraphExecDestroy(s.exec));
-    s.exec = nullptr;
-  }
   const std::int64_t l0 = c.launches;
   cudaGraph_t g = nullptr;
   bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -521,7 +528,7 @@ void run_segment(Ctx& c, const std::uint64_t* key, bool graphable, F&& launches)
       ok = false;
     }
     ok = cudaStreamEndCapture(c.stream, &g) == cudaSuccess && ok;
-    ok = ok && cudaGraphInstantiate(&s.exec, g, 0) == cudaSuccess;
+    ok = ok && install_graph(s.exec, g);
     if (g) cudaGraphDestroy(g);
   }
   if (ok) {
