@@ -365,6 +365,7 @@ void unpack_velocities(Ctx& c) {
 
 void unsort(Ctx& c) {
   c.near_ok = false;   // slots change: the near list no longer describes them
+  c.center_slots = -1;   // (identity order: no slot-class truncation of the launches)
   if (!c.sorted || c.n == 0) {
     c.sorted = false;
     return;
