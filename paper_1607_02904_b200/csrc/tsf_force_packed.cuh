@@ -161,10 +161,12 @@ __device__ __forceinline__ void packed_work(const ForceArgs<R>& a,
       P.foreign = FOREIGN && __shfl_sync(kFull, fgn, k);
       P.ni = P.slot ? nk : 0;
       P.gl = lane - P.h;
-      TSF_DCHECK(P.h >= 0 && P.h <= lane && P.ai >= 0 && P.ai <= last, "k_force_packed segment head");
+      TSF_DCHECK(!heads || (P.h >= 0 && P.h <= lane && P.ai >= 0 && P.ai <= last),
+                 "k_force_packed segment head");
       TSF_DCHECK(!P.slot || (P.gl < P.ni && P.ni <= 32), "k_force_packed segment slot");
       P.v = P.slot ? a.nbr[ell_at(P.gl, P.ai, a.npad)] : P.ai;
     };
+    if (total == 0) return;                       // warp-uniform: no slot in the chunk
     PackLane cur;
     pack_at(0, __popc(__ballot_sync(kFull, n == 0)), cur);
     double4 pi_c, pj_c;
