@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
                    Acc(rx * py), Acc(rx * pz), Acc(ry * pz)};
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
-        if (!slot || (FOREIGN && foreign)) ev[q] = Acc(0);
+        if (!slot || (FOREIGN && foreign) || (!VIR && q > 0)) ev[q] = Acc(0);
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) ev[q] += __shfl_xor_sync(kFull, ev[q], o);
       }

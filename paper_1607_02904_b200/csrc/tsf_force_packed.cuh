@@ -339,10 +339,11 @@ __device__ __forceinline__ void packed_work(const ForceArgs<R>& a,
       }
       if constexpr (OVF && DET) {
         const bool cnt_ev = slot && !(FOREIGN && foreign);
+        const bool cnt_w = cnt_ev && VIR;   // (virial-free callers: zeros)
         s_seg[3][tid] = cnt_ev ? Acc(vv) : Acc(0);
-        s_seg[4][tid] = cnt_ev ? Acc(rx * px) : Acc(0);
-        s_seg[5][tid] = cnt_ev ? Acc(ry * py) : Acc(0);
-        s_seg[6][tid] = cnt_ev ? Acc(rz * pz) : Acc(0);
+        s_seg[4][tid] = cnt_w ? Acc(rx * px) : Acc(0);
+        s_seg[5][tid] = cnt_w ? Acc(ry * py) : Acc(0);
+        s_seg[6][tid] = cnt_w ? Acc(rz * pz) : Acc(0);
         // the three off-diagonal components follow in a second round below
       }
       __syncwarp();
@@ -365,10 +366,10 @@ __device__ __forceinline__ void packed_work(const ForceArgs<R>& a,
       }
       if constexpr (OVF && DET) {
         __syncwarp();
-        const bool cnt_ev = slot && !(FOREIGN && foreign);
-        s_seg[3][tid] = cnt_ev ? Acc(rx * py) : Acc(0);
-        s_seg[4][tid] = cnt_ev ? Acc(rx * pz) : Acc(0);
-        s_seg[5][tid] = cnt_ev ? Acc(ry * pz) : Acc(0);
+        const bool cnt_w = slot && !(FOREIGN && foreign) && VIR;
+        s_seg[3][tid] = cnt_w ? Acc(rx * py) : Acc(0);
+        s_seg[4][tid] = cnt_w ? Acc(rx * pz) : Acc(0);
+        s_seg[5][tid] = cnt_w ? Acc(ry * pz) : Acc(0);
         __syncwarp();
         if (head)
           for (int u = 0; u < ni; ++u) {

@@ -133,6 +133,38 @@ def test_deterministic_mode_is_bitwise_reproducible(tb, sic_text):
         ctx.close()
 
 
+def test_virial_free_kernels_match(tb, sic_text):
+    """TSF_NO_VIRIAL / a NULL virial next to energy or forces selects kernels
+    that never form the virial (the MD loop and the drop-in shim use them):
+    in deterministic mode energy and forces are bitwise those of the full
+    kernels — the G = 4 main launch, the packed main launch (SiC) and the
+    packed tier (a liquid-like system at G = 4) — and the device virial is
+    zero; all three precisions."""
+    from paper_1607_02904_b200 import _lib as L
+    import ctypes as C
+    cases = [systems.perturbed(tb, 4, 0.12, 52, skin=0.5), systems.liquid_like(tb, 4, 0.35, 5),
+             systems.zincblende(tb, sic_text, 4, jitter=0.1)]
+    for case in cases:
+        _, ctx = _ctx(tb, case)
+        for prec in ("double", "mixed", "single"):
+            e1, f1, w1 = ctx.compute(prec, deterministic=True)
+            e2, f2, w2 = ctx.compute(prec, deterministic=True, virial=False)
+            assert w2 is None and e1 == e2 and np.array_equal(f1, f2), (case.name, prec)
+            e3, f3, _ = ctx.compute(prec, deterministic=True, energy=True, forces=True,
+                                    virial=False, form_virial=False)
+            assert e1 == e3 and np.array_equal(f1, f3)
+            ctx.compute(prec, deterministic=True, energy=False, forces=False, virial=False,
+                        form_virial=False)
+            import torch
+            d = torch.empty(7, dtype=torch.float64, device="cuda:0")
+            ctx._ok(L.lib().tsf_results_device(ctx._h, C.c_void_p(d.data_ptr()), None))
+            torch.cuda.synchronize()
+            ev = d.cpu().numpy()
+            assert ev[0] == e1 and np.all(ev[1:] == 0.0), (case.name, prec, ev)
+            assert np.abs(w1).max() > 0
+        ctx.close()
+
+
 def test_filter_off_matches_filter_on(tb, oracle):
     """Acceptance criterion 5 (acceptance.cpp:195-230): 1e-12 relative."""
     case = systems.perturbed(tb, 4, 0.12, 52, skin=0.5)
