@@ -403,8 +403,6 @@ template <bool MULTI>
 __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands& fb, int at,
                                            const int* __restrict__ L, int m, int pre,
                                            int* __restrict__ out) {
-  const float4 pfa = a.posf[at];
-  const int si = MULTI ? min(max(int(pfa.w), 0), fb.ns - 1) : 0;
   int4 e[4];
   // streamed once per step: evict-first keeps the gathered shadow in L2.
   // Loaded without waiting for the count (every list has >= 16 allocated
@@ -434,6 +432,8 @@ __device__ __forceinline__ int filter_list(const ListArgs& a, const FilterBands&
       return m;
     }
   }
+  const float4 pfa = a.posf[at];   // (after the all-sure copy, which needs none)
+  const int si = MULTI ? min(max(int(pfa.w), 0), fb.ns - 1) : 0;
   // test all of them before any store or exact fallback: nothing between the
   // gathers keeps the compiler from issuing them back to back
   unsigned keep = 0, uns = 0;
@@ -555,13 +555,24 @@ __global__ void __launch_bounds__(kBlock, TSF_FILTER_MINB) k_filter(
   const int at = slot_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (at >= slot_hi) return;
   // the force accumulator of the atomic-mode kernel that follows, zeroed here
-  // (this thread is waiting on its list anyway) instead of by a memset
-  if (zero_bytes == 8) {
-    double* z = static_cast<double*>(zero_f) + 3 * std::size_t(at);
-    z[0] = z[1] = z[2] = 0.0;
-  } else if (zero_bytes == 4) {
-    float* z = static_cast<float*>(zero_f) + 3 * std::size_t(at);
-    z[0] = z[1] = z[2] = 0.0f;
+  // (this thread is waiting on its list anyway) instead of by a memset: the
+  // launch's 3 (hi - lo) words, thread g taking words g, g + m, g + 2m —
+  // three fully coalesced stores (a stride-3 triple per thread left each
+  // store instruction a third of its sectors)
+  if (zero_bytes) {
+    const std::size_t m = std::size_t(slot_hi - slot_lo);
+    const std::size_t w = 3 * std::size_t(slot_lo) + std::size_t(at - slot_lo);
+    if (zero_bytes == 8) {
+      double* z = static_cast<double*>(zero_f) + w;
+      z[0] = 0.0;
+      z[m] = 0.0;
+      z[2 * m] = 0.0;
+    } else {
+      float* z = static_cast<float*>(zero_f) + w;
+      z[0] = 0.0f;
+      z[m] = 0.0f;
+      z[2 * m] = 0.0f;
+    }
   }
   // grid-uniform: the smallest near list no atom has moved far enough since
   // the build to invalidate (Ctx::near_list), else the skin list
