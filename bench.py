@@ -317,11 +317,12 @@ def cpu_baseline(text, xyz, species, box, per, masses):
             "sample": f"compute_ref (1 thread) on the full {n}-atom system, one call, {t:.2f} s"}
 
 
-def md_leg(tb, params, args):
+def md_leg(tb, params, args, precision=None):
     """NVE MD steps through tsf_md_run on the workload's lattice at 1600 K
     (init_velocities seed 12345, dt 1 fs, skin 1 A, thermo every 100 steps):
     W warm-up steps, then max(100, K) timed steps including every rebuild."""
     import torch
+    prec = precision or args.precision
     cells = CONFIGS[args.config][0]
     s = tb.make_diamond_lattice(*cells, CONFIGS[args.config][1])
     tb.init_velocities(s, 1600.0, 12345)
@@ -330,14 +331,14 @@ def md_leg(tb, params, args):
     ctx.build_neighbor_list(params.r_cut_max, 1.0)
     ctx.md_set_state(s.velocities, s.species_masses)
     det = args.deterministic
-    ctx.md_run(max(args.warmup, 20), 0.001, args.precision, det, 100)
+    ctx.md_run(max(args.warmup, 20), 0.001, prec, det, 100)
     steps = max(100, args.steps)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.cuda.current_device())
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
-    thermo, rebuilds = ctx.md_run(steps, 0.001, args.precision, det, 100)
+    thermo, rebuilds = ctx.md_run(steps, 0.001, prec, det, 100)
     e1.record(stream)
     e1.synchronize()
     t = e0.elapsed_time(e1) / 1e3
@@ -346,7 +347,7 @@ def md_leg(tb, params, args):
     n = s.natoms
     return {"metric": "MD atom-steps/s", "value": n * steps / t, "unit": UNIT,
             "ms_per_step": 1e3 * t / steps, "steps": steps, "rebuilds": int(rebuilds),
-            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": args.precision,
+            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": prec,
             "scatter": "deterministic gather" if det else "atomics",
             "workload": f"{CONFIGS[args.config][4]}, perfect lattice + init_velocities(1600 K, "
                         "seed 12345), dt 1 fs, skin 1 A, needs_rebuild every step, thermo "
@@ -405,7 +406,7 @@ def md_leg_dd(tb, params, args, world, rank, local):
     return {"metric": "MD atom-steps/s", "value": n * steps / t, "unit": UNIT,
             "ms_per_step": 1e3 * t / steps, "steps": steps, "rebuilds": int(rebuilds),
             "atoms_migrated_rank0": int(migrated),
-            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": args.precision,
+            "ns_per_day": steps * 1e-6 / t * 86400.0, "precision": prec,
             "scatter": "deterministic gather" if det else "atomics",
             "workload": f"{CONFIGS[args.config][4]}, perfect lattice + init_velocities(1600 K, "
                         f"seed 12345), dt 1 fs, skin 1 A, {world} x slabs (tsf_dd_md_run: "
@@ -684,6 +685,13 @@ def main():
     if not args.no_md and args.config in ("si2m", "si32k"):
         md = md_leg_dd(tb, params, args, world, rank, local) if use_dec else \
             md_leg(tb, params, args)
+        if md and not use_dec and not args.no_variants:
+            # the paper's other precisions on the same MD workload
+            md["variants"] = {}
+            for prec in [p for p in DTYPES if p != args.precision]:
+                v = md_leg(tb, params, args, prec)
+                md["variants"][prec] = {k: v[k] for k in ("value", "ms_per_step", "rebuilds",
+                                                          "rel_energy_drift")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
