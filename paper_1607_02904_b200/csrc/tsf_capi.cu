@@ -163,6 +163,7 @@ void set_geometry(Ctx& c, std::int64_t n, const double* box, const std::uint8_t*
     c.boxf.len[ax] = float(box[ax]);
     c.boxf.half[ax] = 0.5f * float(box[ax]);
     c.boxf.per[ax] = c.box.per[ax];
+    c.boxf.inv[ax] = c.box.per[ax] ? 1.0f / c.boxf.len[ax] : 0.0f;
   }
   if (n != c.n) {
     c.n = n;
