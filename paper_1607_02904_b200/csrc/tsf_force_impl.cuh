@@ -788,14 +788,19 @@ __global__ void __launch_bounds__(kBlock) k_gather(int n, int npad, const int* _
     const int b = nbr[ell_at(s, a, npad)];
     TSF_DCHECK(b >= 0 && b < n && b != a, "k_gather list entry");
     const int mb = cnt[b];
-    for (int t = 0; t < mb; ++t) {
-      if (nbr[ell_at(t, b, npad)] == a) {
-        const std::size_t q = std::size_t(t) * npad + b;
-        fx += sx[q];
-        fy += sy[q];
-        fz += sz[q];
-        break;
-      }
+    // a's position in b's list, four entries per 128-bit load (one ELL4
+    // block; the scalar search took ~2.5 dependent loads per neighbour)
+    int t = -1;
+    for (int t0 = 0; t0 < mb && t < 0; t0 += 4) {
+      const int4 e = *reinterpret_cast<const int4*>(nbr + ell_at(t0, b, npad));
+      const int k = e.x == a ? 0 : e.y == a ? 1 : e.z == a ? 2 : e.w == a ? 3 : 4;
+      if (k < 4 && t0 + k < mb) t = t0 + k;
+    }
+    if (t >= 0) {
+      const std::size_t q = std::size_t(t) * npad + b;
+      fx += sx[q];
+      fy += sy[q];
+      fz += sz[q];
     }
   }
   out[3 * std::size_t(a)] = double(fx);
