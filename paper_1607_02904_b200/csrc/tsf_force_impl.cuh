@@ -503,14 +503,15 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         if (kRolled) break;
         continue;
       }
-      int m = gl + t;
-      if (m >= n_i) m -= n_i;
+      int m = gl + t;   // G = 4: (l + t) mod 4 whatever n_i <= 4 (empty slots: meta masks them)
+      if (G == 4) m &= 3;
+      else if (m >= n_i) m -= n_i;
       const int src = gbase + (m & (G - 1));
       Nbr<R> k;
       R fck, dfck;
       int kmeta;
       st.get(src, k, fck, dfck, kmeta);
-      bool ok = pair_ok && t < n_i && kmeta >= 0;
+      bool ok = pair_ok && (G == 4 || t < n_i) && kmeta >= 0;
       const Row<R>* prow = &pjj;
       if (SPEC != kSingle) {
         const int sk = max(kmeta, 0);
@@ -569,14 +570,15 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         sc = ckc[t] * dvdz;
         sd = ckd[t] * dvdz;
       } else {
-        int m = gl + t;
-        if (m >= n_i) m -= n_i;
+        int m = gl + t;   // G = 4: (l + t) mod 4 whatever n_i <= 4 (empty slots: meta masks them)
+        if (G == 4) m &= 3;
+        else if (m >= n_i) m -= n_i;
         const int src = gbase + (m & (G - 1));
         Nbr<R> k;
         R fck, dfck;
         int kmeta;
         st.get(src, k, fck, dfck, kmeta);
-        bool ok = pair_ok && t < n_i && kmeta >= 0;
+        bool ok = pair_ok && (G == 4 || t < n_i) && kmeta >= 0;
         const Row<R>* prow = &pjj;
         if (SPEC != kSingle) {
           const int sk = max(kmeta, 0);
@@ -593,7 +595,8 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
         sd = tr.D * dvdz;
       }
       int s = gl - t;
-      if (s < 0) s += n_i;
+      if (G == 4) s &= 3;
+      else if (s < 0) s += n_i;
       const int from = s & (G - 1);
       const R rc = __shfl_sync(kFull, sc, wbase + from);
       alpha += __shfl_sync(kFull, sd, wbase + from);
