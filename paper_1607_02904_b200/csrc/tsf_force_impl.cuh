@@ -483,7 +483,14 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     // With the ramp (and so the cutoff) fixed by (i, k), "usable as k" is
     // exactly "pair (i, k) inside its own cutoff".
     const int meta = SPEC == kGeneric ? (slot ? sj : -1) : (pair_ok ? sj : -1);
-    st.put(tid, me, fc, dfc, meta);
+    // single species at G = 4 (kNoMask): a slot that is no usable k stages
+    // f_C = f_C' = 0, so its triplets are exact zeros without a mask — and
+    // a lane whose own pair is out has dV/dzeta = 0, which zeroes everything
+    // its triplets send (every exponential argument is bounded: dispatch
+    // requires Row::exp_ok for kSingle)
+    constexpr bool kNoMask = SPEC == kSingle && G == 4;
+    if (kNoMask) st.put(tid, me, pair_ok ? fc : R(0), pair_ok ? dfc : R(0), meta);
+    else st.put(tid, me, fc, dfc, meta);
     if (SPEC == kGeneric) s_r2[tid] = r2;
     __syncwarp();
 
@@ -521,9 +528,12 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
           cutoff_ramp(k.r, *prow, fck, dfck);
         }
       }
-      fck = ok ? fck : R(0);
-      dfck = ok ? dfck : R(0);
-      const Grad<R> tr = triplet<R, (SPEC == kSingle ? 1 : -1), EXPNB>(me, k, fck, dfck, ok, *prow);
+      if (!kNoMask) {
+        fck = ok ? fck : R(0);
+        dfck = ok ? dfck : R(0);
+      }
+      const Grad<R> tr =
+          triplet<R, (SPEC == kSingle ? 1 : -1), EXPNB>(me, k, fck, dfck, kNoMask || ok, *prow);
       zeta += tr.z;
       sb += tr.B;
       gjx += k.ux * tr.A;
@@ -1072,8 +1082,10 @@ void run_force(Ctx& c, const ForceArgs<R>& a, bool vir) {
 template <typename R, typename Acc, bool DET>
 void dispatch_spec(Ctx& c, const ForceArgs<R>& a, bool vir) {
   // kSingle compiles the cubic triplet exponent in (every single-species
-  // table in use has m = 3); a single-species m = 1 table takes kHoist
-  if (c.params.species_count() == 1 && c.params.entry(0, 0, 0).m == 3)
+  // table in use has m = 3) and drops the triplet masks at G = 4, which needs
+  // every exponential argument within a cutoff bounded (Row::exp_ok); other
+  // single-species tables take kHoist
+  if (c.params.species_count() == 1 && c.params.entry(0, 0, 0).m == 3 && a.row0.exp_ok != R(0))
     run_force<R, Acc, kSingle, DET>(c, a, vir);
   else if (c.hoist_ramp) run_force<R, Acc, kHoist, DET>(c, a, vir);
   else run_force<R, Acc, kGeneric, DET>(c, a, vir);
