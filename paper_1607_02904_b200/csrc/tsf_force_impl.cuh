@@ -556,7 +556,9 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
       v = R(0.5) * fc * rep;
       dvdr = R(0.5) * (dfc * rep + fc * (dfr + b * dfa));
       dvdz = R(0.5) * fc * fa * db;
-      if (!isfinite(v) || !isfinite(dvdr) || !isfinite(dvdz)) atomicOr(a.flags, kErrNonFinite);
+      // one test: a non-finite term makes the sum non-finite (the terms are
+      // far below the range where finite ones could overflow it)
+      if (!isfinite(v + dvdr + dvdz)) atomicOr(a.flags, kErrNonFinite);
     }
     // P_l = -(u_l (dV/dr + dV/dzeta sum B + sum_s D_s) + dV/dzeta sum(u_k A)
     //        + sum_s u_s C_s), s over the lanes whose k is l
@@ -619,7 +621,9 @@ __global__ void __launch_bounds__(kBlock, (kForceMinBlocks<R, G>))
     px -= me.ux * alpha;
     py -= me.uy * alpha;
     pz -= me.uz * alpha;
-    if (!slot) px = py = pz = 0;
+    // (kNoMask: an empty slot's P is already +-0 — dV/dzeta = 0 and every
+    // sender's coefficients for it carry its staged f_C = 0)
+    if (!kNoMask && !slot) px = py = pz = 0;
 
     // F_i = -sum over the group's slots
     R fx = px, fy = py, fz = pz;
