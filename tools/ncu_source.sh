@@ -8,7 +8,7 @@ mkdir -p $OUT
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-variants $@"
 $B > $OUT/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    --nvtx --nvtx-include "bench_steps/" -k "regex:$K" -c 1 -o /tmp/prof_$TAG $B > $OUT/ncu.log 2>&1
+    --nvtx --nvtx-include "bench_steps/" -k "regex:$K" -c 1 -f -o /tmp/prof_$TAG $B > $OUT/ncu.log 2>&1
 echo "ncu $TAG rc=$?"
 ncu -i /tmp/prof_$TAG.ncu-rep --page raw --csv > $OUT/raw.csv
 ncu -i /tmp/prof_$TAG.ncu-rep --page details --csv > $OUT/details.csv
