@@ -287,7 +287,8 @@ __device__ __forceinline__ void packed_work(const ForceArgs<R>& a,
         vv = R(0.5) * fc * rep;
         dvdr = R(0.5) * (dfc * rep + fc * (dfr + b * dfa));
         dvdz = R(0.5) * fc * fa * db;
-        if (!isfinite(vv) || !isfinite(dvdr) || !isfinite(dvdz)) atomicOr(a.flags, kErrNonFinite);
+        // one test, as in k_force: a non-finite term makes the sum non-finite
+        if (!isfinite(vv + dvdr + dvdz)) atomicOr(a.flags, kErrNonFinite);
       }
       R alpha = dvdr + dvdz * sb;
       R px = -(gjx * dvdz);
