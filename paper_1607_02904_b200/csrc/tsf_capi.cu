@@ -160,6 +160,7 @@ void set_geometry(Ctx& c, std::int64_t n, const double* box, const std::uint8_t*
     geometry_changed |= c.box.len[ax] != box[ax] || c.box.per[ax] != int(per[ax] != 0);
     c.box.len[ax] = box[ax];
     c.box.per[ax] = per[ax] != 0;
+    c.box.quarter[ax] = 0.25 * box[ax];
     c.boxf.len[ax] = float(box[ax]);
     c.boxf.half[ax] = 0.5f * float(box[ax]);
     c.boxf.per[ax] = c.box.per[ax];

@@ -38,6 +38,7 @@ constexpr int kBlock = 128;             // threads per block, force + list kerne
 struct Box {
   double len[3];
   int per[3];
+  double quarter[3];   // len / 4 (exact), min_image's no-wrap bound (set_geometry)
 };
 
 // Reference cell grid (neighbor.cpp:50-77): edge >= cutoff + skin.  Atoms are
@@ -57,8 +58,8 @@ __device__ __forceinline__ double min_image_exact(double d, double len) {
 // Bitwise the same value as min_image_exact.  |d| <= L/4 gives
 // floor(d/L + 0.5) == 0 under any rounding, hence d itself, so the divide
 // only runs for displacements that cross a periodic face.
-__device__ __forceinline__ double min_image(double d, double len) {
-  if (fabs(d) <= 0.25 * len) return d;
+__device__ __forceinline__ double min_image(double d, double len, double quarter) {
+  if (fabs(d) <= quarter) return d;
   return min_image_exact(d, len);
 }
 
@@ -72,9 +73,9 @@ __device__ __forceinline__ void displacement(const double4& a, const double4& b,
   dx = __dsub_rn(b.x, a.x);
   dy = __dsub_rn(b.y, a.y);
   dz = __dsub_rn(b.z, a.z);
-  if (box.per[0]) dx = min_image(dx, box.len[0]);
-  if (box.per[1]) dy = min_image(dy, box.len[1]);
-  if (box.per[2]) dz = min_image(dz, box.len[2]);
+  if (box.per[0]) dx = min_image(dx, box.len[0], box.quarter[0]);
+  if (box.per[1]) dy = min_image(dy, box.len[1], box.quarter[1]);
+  if (box.per[2]) dz = min_image(dz, box.len[2], box.quarter[2]);
 }
 
 __device__ __forceinline__ int species_of(const double4& p) { return int(p.w); }
